@@ -1,0 +1,205 @@
+/*
+ * csd_b200.h — C ABI of the B200-native Chipmunk column-sparse-delta path.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and status codes, no
+ * C++/torch types.  Every entry point replaces one routine of the reference's
+ * C++ operator API (namespace csd, /root/reference/proj/include/csd/*.hpp);
+ * the replaced declaration is cited on each function.  The host-side C++
+ * mirror of that API (include/csd/*.hpp, libcsd_host.so) and the Python
+ * binding (paper_2506_03275_b200/_capi.py) are both thin layers over this.
+ *
+ * Conventions
+ *  - Tensor pointers are DEVICE pointers (cudaMalloc / torch CUDA storage),
+ *    row-major, in the reference's layouts unless a `layout` argument says
+ *    otherwise.  `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *    default stream).  Calls are stream-ordered and asynchronous except
+ *    where noted; validation that needs device data (index uniqueness,
+ *    non-finite logits) happens in-kernel and is reported by csd_ctx_sync().
+ *  - mode CSD_MODE_CHECK: fp32 storage, bit-exact reproduction of the
+ *    reference arithmetic (sequential fp32 accumulation, no FMA contraction,
+ *    glibc-2.39-compatible expf/tanhf).  Any shape the reference accepts.
+ *  - mode CSD_MODE_PROD: bf16 activations/weights, fp32 accumulation on
+ *    tcgen05 tensor cores (TMEM accumulators, TMA-gathered operand tiles).
+ *    Shapes outside a kernel's envelope return CSD_ERR_UNSUPPORTED — there is
+ *    no CPU or eager fallback.
+ *  - Index sets follow SparseIndexSet (sparse_index.hpp:15-40): indices
+ *    int32 [rows * k_max], counts int32 [rows], rows = B*H*C (H = 1 for MLP).
+ *  - Errors: a csd_status; csd_last_error() returns a thread-local message
+ *    naming the offending value, mirroring the reference exception text.
+ */
+#ifndef CSD_B200_H
+#define CSD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSD_ABI_VERSION 1
+
+/* Status codes <-> reference exception classes (error.hpp:8-46). */
+typedef enum {
+    CSD_OK = 0,
+    CSD_ERR_SHAPE = 1,       /* ShapeError   */
+    CSD_ERR_INDEX = 2,       /* IndexError   */
+    CSD_ERR_NUMERIC = 3,     /* NumericError */
+    CSD_ERR_STATE = 4,       /* StateError   */
+    CSD_ERR_VALUE = 5,       /* ValueError   */
+    CSD_ERR_CONFIG = 6,      /* ConfigError  */
+    CSD_ERR_CUDA = 7,        /* CUDA runtime / launch failure */
+    CSD_ERR_UNSUPPORTED = 8  /* shape outside the production kernel envelope */
+} csd_status;
+
+typedef enum { CSD_MODE_CHECK = 0, CSD_MODE_PROD = 1 } csd_mode;
+
+/* Attention tensor layouts: reference [B,H,N,E] or token-major [B,N,H,E]
+ * (what a fused x@Wq projection produces; avoids split/merge_heads copies,
+ * model.cpp:122-165). */
+typedef enum { CSD_LAYOUT_BHNE = 0, CSD_LAYOUT_BNHE = 1 } csd_layout;
+
+typedef struct csd_ctx csd_ctx;
+
+int csd_abi_version(void);
+const char* csd_last_error(void);
+const char* csd_status_name(csd_status s);
+
+/* Context: device binding, scratch workspace, side stream, error flag. */
+csd_status csd_ctx_create(int device, csd_ctx** out);
+csd_status csd_ctx_destroy(csd_ctx* ctx);
+/* Synchronises `stream` and surfaces in-kernel validation failures
+ * (duplicate / out-of-range ids, non-finite logits) as the matching status. */
+csd_status csd_ctx_sync(csd_ctx* ctx, void* stream);
+/* Number of kernels this context launched since creation (instrumentation). */
+int64_t csd_ctx_launch_count(const csd_ctx* ctx);
+
+/* ---------------------------------------------------------------- voxel --
+ * voxel.hpp:30-36.  The permutation is computed on the host; the device
+ * reorder derives it arithmetically per row (no index array in HBM).      */
+/* voxel_permutation (voxel.cpp:18-42): perm_out[N] on the HOST. */
+csd_status csd_voxel_permutation(int64_t t, int64_t h, int64_t w, int64_t vt, int64_t vh,
+                                 int64_t vw, int64_t* perm_out);
+/* voxel_order (inverse=0, voxel.cpp:44-73) / reverse_voxel_order (inverse=1,
+ * voxel.cpp:75-102) for rows of `row_bytes` bytes (any dtype; bit-exact). */
+csd_status csd_voxel_reorder(csd_ctx* ctx, const void* src, void* dst, int64_t batch, int64_t t,
+                             int64_t h, int64_t w, int64_t vt, int64_t vh, int64_t vw,
+                             int64_t row_bytes, int inverse, void* stream);
+
+/* ---------------------------------------------------------------- top-k --
+ * select_top_k (sparse_index.hpp:45, sparse_index.cpp:64-96): per row of m
+ * fp32 scores keep the k largest, lower index first on ties, stored in
+ * descending-score order; counts[row] = k.  Exact in both modes. */
+csd_status csd_select_top_k(csd_ctx* ctx, const float* scores, int64_t rows, int64_t m, int64_t k,
+                            int32_t* idx, int32_t* counts, void* stream);
+/* SparseIndexSet::validate (sparse_index.cpp:27-62), on device. */
+csd_status csd_validate_index_set(csd_ctx* ctx, const int32_t* idx, const int32_t* counts,
+                                  int64_t rows, int64_t k_max, int64_t domain, void* stream);
+
+/* ------------------------------------------------------------ attention --
+ * dtype: CHECK -> float tensors; PROD -> bf16 q/k/v/out/base, fp32 stats. */
+/* dense_attention (attention.hpp:30-33, attention.cpp:59-74). */
+csd_status csd_dense_attention(csd_ctx* ctx, csd_mode mode, csd_layout layout, const void* q,
+                               const void* k, const void* v, int64_t batch, int64_t heads,
+                               int64_t n, int64_t e, void* out, void* stream);
+/* column_sum_attention (attention.hpp:35-41, attention.cpp:76-145).
+ * prev_m/prev_l [B,H,N] may be NULL (fresh stats).  Outputs: out, row_max,
+ * exp_sum [B,H,N] (fp32) and column_sums [B,H,N/chunk,N] (fp32). */
+csd_status csd_column_sum_attention(csd_ctx* ctx, csd_mode mode, csd_layout layout,
+                                    const void* q, const void* k, const void* v,
+                                    const float* prev_m, const float* prev_l, int64_t batch,
+                                    int64_t heads, int64_t n, int64_t e, int64_t chunk, void* out,
+                                    float* row_max, float* exp_sum, float* column_sums,
+                                    void* stream);
+/* sparse_delta_attention (attention.hpp:43-47, attention.cpp:147-194):
+ * out = base + scale * softmax(q_c K_S^T / sqrt(E)) V_S per chunk; count 0
+ * chunks copy base bit-exactly.  base may alias out. */
+csd_status csd_sparse_delta_attention(csd_ctx* ctx, csd_mode mode, csd_layout layout,
+                                      const void* q, const void* k, const void* v,
+                                      const int32_t* idx, const int32_t* counts, int64_t k_max,
+                                      int64_t chunk, const void* base, float scale,
+                                      int64_t batch, int64_t heads, int64_t n, int64_t e,
+                                      void* out, void* stream);
+
+/* ------------------------------------------------------------------ MLP --
+ * Weights: w1, w2 [F,D] (neuron-major, mlp.hpp:12-21), b1 [F], b2 [D].
+ * CHECK: all fp32.  PROD: x/w1/w2 bf16, biases fp32, act cache bf16 in the
+ * chunk-major layout [B, N/c, F, c], output cache fp32 [B,N,D]. */
+/* dense_mlp (mlp.hpp:44, mlp.cpp:49-81).  act_out (nullable) receives the
+ * activations in the mode's act-cache layout. */
+csd_status csd_dense_mlp(csd_ctx* ctx, csd_mode mode, const void* x, const void* w1,
+                         const float* b1, const void* w2, const float* b2, int64_t batch,
+                         int64_t n, int64_t d, int64_t f, int64_t chunk, float* out,
+                         void* act_out, void* stream);
+/* mlp_tile_means (mlp.hpp:47, mlp.cpp:83-96): out [B, N/c, F] fp32. */
+csd_status csd_mlp_tile_means(csd_ctx* ctx, csd_mode mode, const void* x, const void* w1,
+                              int64_t batch, int64_t n, int64_t d, int64_t f, int64_t chunk,
+                              float* out, void* stream);
+/* mlp_change_indices (mlp.hpp:51-53, mlp.cpp:98-118). */
+csd_status csd_mlp_change_indices(csd_ctx* ctx, csd_mode mode, const void* x, const void* w1,
+                                  const float* tile_means, int64_t batch, int64_t n, int64_t d,
+                                  int64_t f, int64_t k, int64_t chunk, int32_t* idx,
+                                  int32_t* counts, void* stream);
+/* sparse_delta_mlp (mlp.hpp:55-60, mlp.cpp:120-182): act_cache and
+ * out_cache updated in place (O = O_cache + delta); out (nullable) gets a
+ * copy of the new output in the mode's activation dtype. */
+csd_status csd_sparse_delta_mlp(csd_ctx* ctx, csd_mode mode, const void* x, const void* w1,
+                                const float* b1, const void* w2, const int32_t* idx,
+                                const int32_t* counts, int64_t k_max, int64_t chunk,
+                                int64_t batch, int64_t n, int64_t d, int64_t f, void* act_cache,
+                                float* out_cache, void* stream);
+/* Convert a mode's act cache to the reference layout [B,N,F] fp32 (for the
+ * host mirror's MlpCache::activations view, test_mlp.cpp:234). */
+csd_status csd_mlp_act_cache_to_ref(csd_ctx* ctx, csd_mode mode, const void* act_cache,
+                                    int64_t batch, int64_t n, int64_t f, int64_t chunk,
+                                    float* out, void* stream);
+
+/* --------------------------------------------------------------- dense ops --
+ * project (model.cpp:107-120): out[B,N,Dout] = x[B,N,D] @ w[D,Dout]; and the
+ * residual add (model.cpp:47-57).  CHECK only (PROD projections live inside
+ * the block runner). */
+csd_status csd_project(csd_ctx* ctx, csd_mode mode, const void* x, const void* w, int64_t batch,
+                       int64_t n, int64_t d, int64_t dout, void* out, void* stream);
+csd_status csd_add(csd_ctx* ctx, csd_mode mode, const void* a, const void* b, int64_t numel,
+                   void* out, void* stream);
+
+/* ---------------------------------------------------------------- block --
+ * One DiT block (model.cpp:178-216: x += attn(x Wq, x Wk, x Wv) Wo;
+ * x += mlp(x)) with device-resident weights and per-layer caches
+ * (AttentionCache / MlpCache, attention.hpp:13-19, mlp.hpp:29-36).
+ * Head / hidden sharding: a block may own heads [head0, head0+heads_local)
+ * and neurons [f0, f0+f_local) (csd_block_config); sharded execution is
+ * driven through csd_block_step_partial (see below). */
+typedef struct {
+    int64_t batch, seq, dim, heads, head_dim, hidden, chunk;
+    int64_t attn_k, mlp_k;   /* per-chunk keys / neurons recomputed */
+    int64_t head0, heads_local, f0, f_local;  /* shard (0, heads, 0, hidden) = whole block */
+} csd_block_config;
+
+typedef struct csd_block csd_block;
+
+/* Weights are HOST fp32 in reference layout (wq..wo [D,D], w1/w2 [F,D],
+ * b1 [F], b2 [D]); the block keeps device copies in the mode's dtype. */
+csd_status csd_block_create(csd_ctx* ctx, csd_mode mode, const csd_block_config* cfg,
+                            const float* wq, const float* wk, const float* wv, const float* wo,
+                            const float* w1, const float* b1, const float* w2, const float* b2,
+                            csd_block** out);
+csd_status csd_block_destroy(csd_block* blk);
+/* model_forward_step for one layer: x_out = block(x_in).  x in the mode's
+ * activation dtype, [B,N,D] device.  dense != 0 refreshes the caches.
+ * static_idx/static_counts (nullable, device) replace the attention top-k
+ * on dense steps (attention.hpp:50-52).  A sparse step before any dense step
+ * returns CSD_ERR_STATE. */
+csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int dense,
+                          const int32_t* static_idx, const int32_t* static_counts,
+                          int64_t static_k_max, void* stream);
+/* Cache views (reference layouts, fp32, device): which = 0 attn residual
+ * [B,H,N,E], 1 row_max, 2 exp_sum [B,H,N], 3 mlp act [B,N,F], 4 mlp out
+ * [B,N,D], 5 tile means [B,C,F]; 6/7 attention / mlp index sets (int32). */
+csd_status csd_block_cache(csd_block* blk, int which, void* out, int32_t* counts_out,
+                           void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CSD_B200_H */

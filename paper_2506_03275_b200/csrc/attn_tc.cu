@@ -1,0 +1,500 @@
+// attn_tc.cu — column-sparse attention on tcgen05 (CSD_MODE_PROD).
+//
+// Replaces sparse_delta_attention (attention.cpp:147-194), dense_attention
+// (:59-74) and the dense-step column sums (:76-145) with ONE kernel family:
+//
+//   work item = (b, h, query chunk c): Q_c is 128- or 256-row (NT = 1 or 2
+//   M-tiles of 128; c = 192 uses 2 tiles with 64 idle rows), keys are the
+//   chunk's index list (sparse) or all N keys (dense baseline / dense step).
+//   For each 128-key block j:
+//     producer warp : TMA gather4 of the selected K and V rows (4 rows per
+//                     instruction, two 64-column 128B-swizzled strips at
+//                     E = 128) — or plain TMA tiles in dense mode;
+//     MMA thread    : S_t = Q_t K_j^T  (tcgen05.mma M128 N128 K16, TMEM acc);
+//     softmax warps : one thread per query row (TMEM lane), online softmax
+//                     over the SUBSET with lazy rescaling (only when the row
+//                     max grows by > 2^8), P_t -> smem bf16 (swizzled);
+//                     optional column sums with stale stats (dense step);
+//     MMA thread    : O_t += P_t V_j  (V as MN-major B operand).
+//   Epilogue: out = base + scale * O / l   (the O = O_cache + delta update,
+//   north_star item 5) and the softmax stats (row max / exp sum).
+//
+// TMEM: S tiles at columns [0, 128*NT), O tiles at [128*NT, 128*NT + E*NT).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace csd {
+namespace dev {
+
+using namespace csd::tc;
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+template <int E, int NT>
+struct AttnLayout {
+    static constexpr int kHalves = E / 64;
+    static constexpr uint32_t kStrip = 128 * 128;  // 128 rows x 128 B
+    static constexpr uint32_t kQ = 0;
+    static constexpr uint32_t kK = kQ + NT * kHalves * kStrip;
+    static constexpr uint32_t kV = kK + kHalves * kStrip;
+    static constexpr uint32_t kP = kV + kHalves * kStrip;
+    static constexpr uint32_t kCs = kP + NT * 2 * kStrip;
+    static constexpr uint32_t kBar = kCs + 2 * 4 * NT * 128 * 4;
+    static constexpr uint32_t kBytes = kBar + 256;
+    static constexpr uint32_t kSmemAlloc = kBytes + 1024;  // manual 1 KB alignment
+    static constexpr uint32_t kThreads = 128 + 128 * NT;
+    static constexpr uint32_t kTmemCols = (NT * 128 + NT * E) <= 256 ? 256 : 512;
+};
+
+struct AttnParams {
+    const int32_t* idx;
+    const int32_t* counts;
+    int64_t k_max;
+    const __nv_bfloat16* base;
+    __nv_bfloat16* out;
+    float scale;
+    float* row_max;
+    float* exp_sum;
+    const float* prev_m;
+    const float* prev_l;
+    float* colsum;
+    int layout;
+    int heads, n, chunk, chunks;
+    float qk_scale_log2;  // log2(e) / sqrt(E)
+};
+
+__device__ __forceinline__ int64_t tok_elem_off(int layout, int64_t b, int64_t h, int64_t tok,
+                                                int heads, int n, int e) {
+    return layout == CSD_LAYOUT_BHNE ? (((b * heads + h) * (int64_t)n) + tok) * e
+                                     : ((b * (int64_t)n + tok) * heads + h) * e;
+}
+
+template <int E, int NT>
+__global__ void __launch_bounds__(AttnLayout<E, NT>::kThreads, 1)
+k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kg,
+          const __grid_constant__ CUtensorMap tm_vg, const AttnParams p) {
+    using L = AttnLayout<E, NT>;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_u32 = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int item = blockIdx.x;
+    const int c = item % p.chunks;
+    const int bh = item / p.chunks;
+    const int b = bh / p.heads, h = bh % p.heads;
+    const bool dense = p.idx == nullptr;
+    const int cnt = dense ? p.n : p.counts[item];
+    const int row_base = p.layout == CSD_LAYOUT_BHNE ? bh * p.n : b * p.n;  // tensor-map row
+    const int col0 = p.layout == CSD_LAYOUT_BHNE ? 0 : h * E;
+    const int q_row0 = row_base + c * p.chunk;
+
+    if (cnt == 0) {  // pass base through (attention.cpp:169)
+        if (p.base != p.out && p.base != nullptr) {
+            for (int r = threadIdx.x; r < p.chunk * (E / 8); r += blockDim.x) {
+                const int row = r / (E / 8), v8 = r % (E / 8);
+                const int64_t off = tok_elem_off(p.layout, b, h, (int64_t)c * p.chunk + row,
+                                                 p.heads, p.n, E) + v8 * 8;
+                *reinterpret_cast<uint4*>(p.out + off) =
+                    *reinterpret_cast<const uint4*>(p.base + off);
+            }
+        }
+        return;
+    }
+    const int nblk = (cnt + 127) / 128;
+
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
+    uint64_t* bar_q = bars + 0;
+    uint64_t* bar_kf = bars + 1;
+    uint64_t* bar_ke = bars + 2;
+    uint64_t* bar_vf = bars + 3;
+    uint64_t* bar_ve = bars + 4;
+    uint64_t* bar_s = bars + 5;
+    uint64_t* bar_p = bars + 6;
+    uint64_t* bar_o = bars + 7;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+    if (threadIdx.x == 0) {
+        mbar_init(bar_q, 1);
+        mbar_init(bar_kf, 1);
+        mbar_init(bar_ke, 1);
+        mbar_init(bar_vf, 1);
+        mbar_init(bar_ve, 1);
+        mbar_init(bar_s, 1);
+        mbar_init(bar_p, 128 * NT);
+        mbar_init(bar_o, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<L::kTmemCols>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            tma_prefetch_desc(&tm_q);
+            tma_prefetch_desc(dense ? &tm_k : &tm_kg);
+            tma_prefetch_desc(dense ? &tm_v : &tm_vg);
+            mbar_arrive_expect_tx(bar_q, NT * L::kHalves * L::kStrip);
+            for (int t = 0; t < NT; ++t)
+                for (int hf = 0; hf < L::kHalves; ++hf)
+                    tma_load_2d(&tm_q, bar_q, smem + L::kQ + (t * L::kHalves + hf) * L::kStrip,
+                                col0 + hf * 64, q_row0 + t * 128);
+        }
+        const int32_t* ids = dense ? nullptr : p.idx + (int64_t)item * p.k_max;
+        for (int j = 0; j < nblk; ++j) {
+            int32_t rows[4];
+            if (!dense) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    int r = j * 128 + lane * 4 + i;
+                    r = r < cnt ? r : cnt - 1;  // pad with a valid row (masked in softmax)
+                    rows[i] = row_base + ids[r];
+                }
+            }
+            // K_j
+            if (j > 0) mbar_wait(bar_ke, (j - 1) & 1);
+            if (lane == 0) mbar_arrive_expect_tx(bar_kf, L::kHalves * L::kStrip);
+            __syncwarp();
+            if (dense) {
+                if (lane == 0)
+                    for (int hf = 0; hf < L::kHalves; ++hf)
+                        tma_load_2d(&tm_k, bar_kf, smem + L::kK + hf * L::kStrip, col0 + hf * 64,
+                                    row_base + j * 128);
+            } else {
+                for (int hf = 0; hf < L::kHalves; ++hf)
+                    tma_gather4(&tm_kg, bar_kf, smem + L::kK + hf * L::kStrip + lane * 512,
+                                col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
+            }
+            // V_j
+            if (j > 0) mbar_wait(bar_ve, (j - 1) & 1);
+            if (lane == 0) mbar_arrive_expect_tx(bar_vf, L::kHalves * L::kStrip);
+            __syncwarp();
+            if (dense) {
+                if (lane == 0)
+                    for (int hf = 0; hf < L::kHalves; ++hf)
+                        tma_load_2d(&tm_v, bar_vf, smem + L::kV + hf * L::kStrip, col0 + hf * 64,
+                                    row_base + j * 128);
+            } else {
+                for (int hf = 0; hf < L::kHalves; ++hf)
+                    tma_gather4(&tm_vg, bar_vf, smem + L::kV + hf * L::kStrip + lane * 512,
+                                col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
+            constexpr uint32_t idO = idesc_bf16(128, E, false, true);
+            const uint32_t sQ = smem_u32(smem + L::kQ), sK = smem_u32(smem + L::kK);
+            const uint32_t sV = smem_u32(smem + L::kV), sP = smem_u32(smem + L::kP);
+            mbar_wait(bar_q, 0);
+            for (int j = 0; j < nblk; ++j) {
+                mbar_wait(bar_kf, j & 1);
+                tc_fence_after();
+                for (int t = 0; t < NT; ++t) {
+#pragma unroll
+                    for (int kk = 0; kk < E / 16; ++kk) {
+                        const uint64_t a = desc_kmajor_sw128(
+                            sQ + (t * L::kHalves + kk / 4) * L::kStrip + (kk % 4) * 32);
+                        const uint64_t bd =
+                            desc_kmajor_sw128(sK + (kk / 4) * L::kStrip + (kk % 4) * 32);
+                        mma_bf16(tmem + t * 128, a, bd, idS, kk > 0 ? 1u : 0u);
+                    }
+                }
+                mma_commit(bar_ke);
+                mma_commit(bar_s);
+                mbar_wait(bar_p, j & 1);
+                mbar_wait(bar_vf, j & 1);
+                tc_fence_after();
+                for (int t = 0; t < NT; ++t) {
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint64_t a =
+                            desc_kmajor_sw128(sP + (t * 2 + kk / 4) * L::kStrip + (kk % 4) * 32);
+                        const uint64_t bd = desc_mnmajor_sw128(sV + kk * 2048, L::kStrip);
+                        mma_bf16(tmem + NT * 128 + t * E, a, bd, idO,
+                                 (j > 0 || kk > 0) ? 1u : 0u);
+                    }
+                }
+                mma_commit(bar_ve);
+            }
+            mma_commit(bar_o);
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ softmax / epilogue
+        const int sw = warp - 4;          // 0 .. 4*NT-1
+        const int t = sw >> 2, quad = warp & 3;
+        const int row_t = quad * 32 + lane;
+        const int crow = t * 128 + row_t;  // row within the chunk
+        const bool row_ok = crow < p.chunk;
+        const bool warp_ok = (t * 128 + quad * 32) < p.chunk;
+        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        const uint32_t tS = tmem + lane_off + t * 128;
+        const uint32_t tO = tmem + lane_off + NT * 128 + t * E;
+        uint8_t* sPt = smem + L::kP + t * 2 * L::kStrip;
+        float* cs_part = reinterpret_cast<float*>(smem + L::kCs);
+        const int64_t tok = (int64_t)c * p.chunk + crow;
+        const bool do_cs = p.colsum != nullptr;
+        float mpl = 0.f, inv_lp = 0.f;
+        if (do_cs && row_ok) {
+            const int64_t si = (int64_t)bh * p.n + tok;
+            mpl = p.prev_m[si] * kLog2e;
+            inv_lp = 1.0f / p.prev_l[si];
+        }
+        if (!warp_ok) {  // idle rows: P rows stay zero for the whole item
+#pragma unroll
+            for (int c16 = 0; c16 < 8; ++c16) {
+                *reinterpret_cast<uint4*>(sPt + sw128_offset(row_t, c16)) = make_uint4(0, 0, 0, 0);
+                *reinterpret_cast<uint4*>(sPt + L::kStrip + sw128_offset(row_t, c16)) =
+                    make_uint4(0, 0, 0, 0);
+            }
+        }
+        float m_run = -INFINITY, m_true = -INFINITY, l_run = 0.f;
+        const float sl2 = p.qk_scale_log2;
+        for (int j = 0; j < nblk; ++j) {
+            mbar_wait(bar_s, j & 1);
+            tc_fence_after();
+            const int ncols = min(128, cnt - j * 128);
+            if (warp_ok) {
+                uint32_t r[32];
+                float mx = -INFINITY;
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    tmem_ld32(tS + cc * 32, r);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float x = (cc * 32 + i < ncols) ? __uint_as_float(r[i]) * sl2 : -INFINITY;
+                        mx = fmaxf(mx, x);
+                    }
+                }
+                m_true = fmaxf(m_true, mx);
+                const bool need = mx > m_run + kRescaleThreshold;
+                const float alpha = need ? exp2f(m_run - mx) : 1.0f;
+                if (need) {
+                    m_run = mx;
+                    l_run *= alpha;
+                }
+                if (j > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+                    for (int oc = 0; oc < E / 32; ++oc) {
+                        tmem_ld32(tO + oc * 32, r);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+                        tmem_st32(tO + oc * 32, r);
+                    }
+                    tmem_st_wait();
+                }
+                const float w = do_cs ? exp2f(m_run - mpl) * inv_lp : 0.f;
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    tmem_ld32(tS + cc * 32, r);
+                    tmem_ld_wait();
+                    float pv[32];
+                    float part = 0.f;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const bool ok = row_ok && (cc * 32 + i < ncols);
+                        pv[i] = ok ? exp2f(__uint_as_float(r[i]) * sl2 - m_run) : 0.f;
+                        part += pv[i];
+                    }
+                    l_run += part;
+                    uint8_t* half = sPt + (cc >> 1) * L::kStrip;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 v;
+                        v.x = pack_bf16x2(pv[q * 8 + 0], pv[q * 8 + 1]);
+                        v.y = pack_bf16x2(pv[q * 8 + 2], pv[q * 8 + 3]);
+                        v.z = pack_bf16x2(pv[q * 8 + 4], pv[q * 8 + 5]);
+                        v.w = pack_bf16x2(pv[q * 8 + 6], pv[q * 8 + 7]);
+                        *reinterpret_cast<uint4*>(half + sw128_offset(row_t, (cc & 1) * 4 + q)) = v;
+                    }
+                    if (do_cs) {
+                        // transpose-reduce the warp's 32x32 block: lane ends with column `lane`
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) pv[i] *= w;
+#pragma unroll
+                        for (int wd = 16; wd >= 1; wd >>= 1) {
+                            const bool upper = (lane & wd) != 0;
+#pragma unroll
+                            for (int i = 0; i < wd; ++i) {
+                                const float send = upper ? pv[i] : pv[i + wd];
+                                const float keep = upper ? pv[i + wd] : pv[i];
+                                pv[i] = keep + __shfl_xor_sync(0xffffffffu, send, wd);
+                            }
+                        }
+                        cs_part[((j & 1) * 4 * NT + sw) * 128 + cc * 32 + lane] = pv[0];
+                    }
+                }
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(bar_p);
+            if (do_cs) {
+                named_bar_sync(1, 128 * NT);
+                const int st = sw * 32 + lane;
+                if (st < 128 && st < ncols) {
+                    float s = 0.f;
+                    for (int wsl = 0; wsl < 4 * NT; ++wsl)
+                        if (wsl * 32 < p.chunk) s += cs_part[((j & 1) * 4 * NT + wsl) * 128 + st];
+                    p.colsum[((int64_t)bh * p.chunks + c) * p.n + j * 128 + st] = s;
+                }
+            }
+        }
+        // ------------------------------------------------------------ epilogue
+        mbar_wait(bar_o, 0);
+        tc_fence_after();
+        if (warp_ok) {
+            const float inv_l = 1.0f / l_run;
+            const int64_t off = tok_elem_off(p.layout, b, h, tok, p.heads, p.n, E);
+#pragma unroll
+            for (int oc = 0; oc < E / 32; ++oc) {
+                uint32_t r[32];
+                tmem_ld32(tO + oc * 32, r);
+                tmem_ld_wait();
+                if (row_ok) {
+                    float o[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r[i]) * inv_l;
+                    if (p.base != nullptr) {
+                        const uint4* bp = reinterpret_cast<const uint4*>(p.base + off + oc * 32);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint4 bv = bp[q];
+                            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bv);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const float2 f = __bfloat1622float2(b2[u]);
+                                o[q * 8 + 2 * u] = f.x + p.scale * o[q * 8 + 2 * u];
+                                o[q * 8 + 2 * u + 1] = f.y + p.scale * o[q * 8 + 2 * u + 1];
+                            }
+                        }
+                    }
+                    uint4* dp = reinterpret_cast<uint4*>(p.out + off + oc * 32);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint4 v;
+                        v.x = pack_bf16x2(o[q * 8 + 0], o[q * 8 + 1]);
+                        v.y = pack_bf16x2(o[q * 8 + 2], o[q * 8 + 3]);
+                        v.z = pack_bf16x2(o[q * 8 + 4], o[q * 8 + 5]);
+                        v.w = pack_bf16x2(o[q * 8 + 6], o[q * 8 + 7]);
+                        dp[q] = v;
+                    }
+                }
+            }
+            if (row_ok && p.row_max != nullptr) {
+                const int64_t si = (int64_t)bh * p.n + tok;
+                p.row_max[si] = m_true * kLn2;
+                p.exp_sum[si] = l_run * exp2f(m_run - m_true);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<L::kTmemCols>(tmem);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Host side: tensor maps through the driver entry point (no -lcuda needed).
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    });
+    return fn;
+}
+
+// 2-D bf16 map [rows][cols] with row pitch `pitch_elems`, box {64, box_rows}, 128 B swizzle.
+bool make_map_bf16(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows,
+                   uint64_t pitch_elems, uint32_t box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {pitch_elems * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+bool attn_tc_supported(int64_t e, int64_t chunk) {
+    return (e == 64 || e == 128) && chunk >= 1 && chunk <= 256;
+}
+
+template <int E, int NT>
+static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
+    using L = AttnLayout<E, NT>;
+    const uint64_t cols = a.layout == CSD_LAYOUT_BHNE ? E : (uint64_t)a.heads * E;
+    const uint64_t rows = a.layout == CSD_LAYOUT_BHNE ? (uint64_t)(a.batch * a.heads * a.n)
+                                                      : (uint64_t)(a.batch * a.n);
+    CUtensorMap tq, tk, tv, tkg, tvg;
+    if (!make_map_bf16(&tq, a.q, cols, rows, cols, 128) ||
+        !make_map_bf16(&tk, a.k, cols, rows, cols, 128) ||
+        !make_map_bf16(&tv, a.v, cols, rows, cols, 128) ||
+        !make_map_bf16(&tkg, a.k, cols, rows, cols, 1) ||
+        !make_map_bf16(&tvg, a.v, cols, rows, cols, 1))
+        return cudaErrorInvalidValue;
+    AttnParams p{};
+    p.idx = a.idx;
+    p.counts = a.counts;
+    p.k_max = a.k_max;
+    p.base = static_cast<const __nv_bfloat16*>(a.base);
+    p.out = static_cast<__nv_bfloat16*>(a.out);
+    p.scale = a.scale;
+    p.row_max = a.row_max;
+    p.exp_sum = a.exp_sum;
+    p.prev_m = a.prev_m;
+    p.prev_l = a.prev_l;
+    p.colsum = a.colsum;
+    p.layout = a.layout;
+    p.heads = (int)a.heads;
+    p.n = (int)a.n;
+    p.chunk = (int)a.chunk;
+    p.chunks = (int)(a.n / a.chunk);
+    p.qk_scale_log2 = kLog2e / std::sqrt((float)E);
+    auto kern = k_attn_tc<E, NT>;
+    cudaError_t err =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
+    if (err != cudaSuccess) return err;
+    const unsigned grid = (unsigned)(a.batch * a.heads * p.chunks);
+    kern<<<grid, L::kThreads, L::kSmemAlloc, s>>>(tq, tk, tv, tkg, tvg, p);
+    return cudaGetLastError();
+}
+
+cudaError_t attn_tc(const AttnTcArgs& a, cudaStream_t s) {
+    if (!attn_tc_supported(a.e, a.chunk)) return cudaErrorNotSupported;
+    if (a.n % a.chunk) return cudaErrorInvalidValue;
+    const bool two = a.chunk > 128;
+    if (a.e == 128) return two ? launch_attn<128, 2>(a, s) : launch_attn<128, 1>(a, s);
+    return two ? launch_attn<64, 2>(a, s) : launch_attn<64, 1>(a, s);
+}
+
+}  // namespace dev
+}  // namespace csd

@@ -1,0 +1,341 @@
+// block.cpp — device-resident DiT block (model_forward_step for one layer,
+// model.cpp:178-216) behind csd_block_*.
+//
+//   q,k,v = x Wq, x Wk, x Wv                 (token-major [B,N,H*E]: no split_heads)
+//   dense : O, m, l, colsum = column_sum_attention(q,k,v, stale m,l)   (attention.cpp:202-215)
+//           idx = top-k(colsum) | static pattern;  resid = O - sparse(idx)
+//   sparse: O = resid + sparse(idx)                                     (attention.cpp:217-218)
+//   x1 = x + O Wo
+//   dense : M = dense_mlp(x1), A = act, T_m = tile_means(x1)             (mlp.cpp:196-205)
+//   sparse: S = top-k |tile_means(x1) - T_m|;  A, M updated by the delta (mlp.cpp:206-210)
+//   x2 = x1 + M
+// CHECK mode runs every op on the bit-exact kernels (fp32); PROD mode keeps
+// activations in bf16, caches in bf16/fp32, and uses the tcgen05 attention.
+#include <cstring>
+#include <vector>
+
+#include "capi_internal.h"
+
+using namespace csd::dev;
+using csd::Ctx;
+using csd::cuda_status;
+using csd::set_error;
+
+#define CSD_TRY(expr)                \
+    do {                             \
+        csd_status _s = (expr);      \
+        if (_s != CSD_OK) return _s; \
+    } while (0)
+#define CSD_CU(expr, where)                                   \
+    do {                                                      \
+        cudaError_t _e = (expr);                              \
+        if (_e != cudaSuccess) return cuda_status(_e, where); \
+    } while (0)
+
+struct csd_block {
+    Ctx* ctx = nullptr;
+    csd_mode mode = CSD_MODE_CHECK;
+    csd_block_config cfg{};
+    std::vector<void*> allocs;
+    // weights
+    void *wq = nullptr, *wk = nullptr, *wv = nullptr, *wo = nullptr, *w1 = nullptr, *w2 = nullptr;
+    float *b1 = nullptr, *b2 = nullptr;
+    // activations
+    void *q = nullptr, *k = nullptr, *v = nullptr, *attn = nullptr, *x_mid = nullptr;
+    float* proj = nullptr;  // [B,N,D] fp32 branch output
+    // caches
+    void* resid = nullptr;
+    float *m[2] = {nullptr, nullptr}, *l[2] = {nullptr, nullptr};
+    int cur = 0;
+    float* colsum = nullptr;
+    int32_t *aidx = nullptr, *acnt = nullptr;
+    int64_t a_kmax = 0;
+    float* tmeans = nullptr;
+    void* act = nullptr;
+    float* mout = nullptr;
+    int32_t *midx = nullptr, *mcnt = nullptr;
+    bool attn_init = false, mlp_init = false;
+    int64_t attn_age = 0, mlp_age = 0;
+
+    void* alloc(size_t bytes) {
+        void* p = nullptr;
+        if (cudaMalloc(&p, bytes < 256 ? 256 : bytes) != cudaSuccess) return nullptr;
+        allocs.push_back(p);
+        return p;
+    }
+    ~csd_block() {
+        for (void* p : allocs) cudaFree(p);
+    }
+};
+
+namespace {
+
+size_t esz(csd_mode m) { return m == CSD_MODE_PROD ? 2 : 4; }
+
+// Upload a host fp32 sub-matrix (rows r0.., cols c0..) in the mode's dtype.
+csd_status upload(csd_block* blk, void** dst, const float* host, int64_t rows, int64_t cols,
+                  int64_t ld, int64_t r0, int64_t c0, bool keep_f32) {
+    const size_t n = (size_t)(rows * cols);
+    std::vector<float> tmp(n);
+    for (int64_t r = 0; r < rows; ++r)
+        std::memcpy(&tmp[r * cols], host + (r0 + r) * ld + c0, sizeof(float) * cols);
+    const bool bf = blk->mode == CSD_MODE_PROD && !keep_f32;
+    void* d = blk->alloc(n * (bf ? 2 : 4));
+    if (!d) return set_error(CSD_ERR_CUDA, "block weight allocation failed");
+    if (bf) {
+        float* staging = nullptr;
+        CSD_CU(cudaMalloc(&staging, n * 4), "cudaMalloc");
+        CSD_CU(cudaMemcpy(staging, tmp.data(), n * 4, cudaMemcpyHostToDevice), "h2d");
+        CSD_CU(prod_cast_f32_bf16(staging, d, (int64_t)n, nullptr), "cast");
+        CSD_CU(cudaDeviceSynchronize(), "sync");
+        cudaFree(staging);
+    } else {
+        CSD_CU(cudaMemcpy(d, tmp.data(), n * 4, cudaMemcpyHostToDevice), "h2d");
+    }
+    *dst = d;
+    return CSD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+csd_status csd_block_create(csd_ctx* ctx, csd_mode mode, const csd_block_config* cfg_in,
+                            const float* wq, const float* wk, const float* wv, const float* wo,
+                            const float* w1, const float* b1, const float* w2, const float* b2,
+                            csd_block** out) {
+    if (!ctx || !cfg_in || !out) return set_error(CSD_ERR_VALUE, "csd_block_create: null argument");
+    csd_block_config c = *cfg_in;
+    if (c.heads_local == 0) c.heads_local = c.heads;
+    if (c.f_local == 0) c.f_local = c.hidden;
+    // model.cpp:10-28 validation
+    if (c.batch < 1 || c.seq < 1 || c.dim < 1 || c.heads < 1 || c.head_dim < 1 || c.hidden < 1 ||
+        c.chunk < 1)
+        return set_error(CSD_ERR_CONFIG, "model config fields must be positive");
+    if (c.dim != c.heads * c.head_dim)
+        return set_error(CSD_ERR_CONFIG, "model_dim %lld != heads*head_dim %lld", (long long)c.dim,
+                         (long long)(c.heads * c.head_dim));
+    if (c.seq % c.chunk)
+        return set_error(CSD_ERR_CONFIG, "sequence length %lld not divisible by chunk %lld",
+                         (long long)c.seq, (long long)c.chunk);
+    if (c.head0 < 0 || c.head0 + c.heads_local > c.heads || c.f0 < 0 || c.f0 + c.f_local > c.hidden)
+        return set_error(CSD_ERR_CONFIG, "shard outside the block");
+    auto* blk = new csd_block;
+    blk->ctx = reinterpret_cast<Ctx*>(ctx);
+    blk->mode = mode;
+    blk->cfg = c;
+    const int64_t B = c.batch, N = c.seq, D = c.dim, E = c.head_dim, Hl = c.heads_local;
+    const int64_t Dl = Hl * E, Fl = c.f_local, C = N / c.chunk;
+    csd_status st = CSD_OK;
+    auto fail = [&](csd_status s) {
+        delete blk;
+        return s;
+    };
+    const int64_t col0 = c.head0 * E;
+    if ((st = upload(blk, &blk->wq, wq, D, Dl, D, 0, col0, false)) != CSD_OK) return fail(st);
+    if ((st = upload(blk, &blk->wk, wk, D, Dl, D, 0, col0, false)) != CSD_OK) return fail(st);
+    if ((st = upload(blk, &blk->wv, wv, D, Dl, D, 0, col0, false)) != CSD_OK) return fail(st);
+    if ((st = upload(blk, &blk->wo, wo, Dl, D, D, col0, 0, false)) != CSD_OK) return fail(st);
+    if ((st = upload(blk, &blk->w1, w1, Fl, D, D, c.f0, 0, false)) != CSD_OK) return fail(st);
+    if ((st = upload(blk, &blk->w2, w2, Fl, D, D, c.f0, 0, false)) != CSD_OK) return fail(st);
+    void* tmp = nullptr;
+    if ((st = upload(blk, &tmp, b1, 1, Fl, Fl, 0, c.f0, true)) != CSD_OK) return fail(st);
+    blk->b1 = (float*)tmp;
+    std::vector<float> b2l(D, 0.0f);
+    if (c.f0 == 0) std::memcpy(b2l.data(), b2, sizeof(float) * D);  // bias once across shards
+    if ((st = upload(blk, &tmp, b2l.data(), 1, D, D, 0, 0, true)) != CSD_OK) return fail(st);
+    blk->b2 = (float*)tmp;
+
+    const size_t es = esz(mode);
+    blk->q = blk->alloc(es * B * N * Dl);
+    blk->k = blk->alloc(es * B * N * Dl);
+    blk->v = blk->alloc(es * B * N * Dl);
+    blk->attn = blk->alloc(es * B * N * Dl);
+    blk->resid = blk->alloc(es * B * N * Dl);
+    blk->x_mid = blk->alloc(es * B * N * D);
+    blk->proj = (float*)blk->alloc(4 * B * N * D);
+    for (int i = 0; i < 2; ++i) {
+        blk->m[i] = (float*)blk->alloc(4 * B * Hl * N);
+        blk->l[i] = (float*)blk->alloc(4 * B * Hl * N);
+    }
+    blk->colsum = (float*)blk->alloc(4 * B * Hl * C * N);
+    const int64_t ak = c.attn_k > 0 ? c.attn_k : N;
+    blk->a_kmax = ak;
+    blk->aidx = (int32_t*)blk->alloc(4 * B * Hl * C * ak);
+    blk->acnt = (int32_t*)blk->alloc(4 * B * Hl * C);
+    blk->tmeans = (float*)blk->alloc(4 * B * C * Fl);
+    blk->act = blk->alloc(es * B * N * Fl);
+    blk->mout = (float*)blk->alloc(4 * B * N * D);
+    const int64_t mk = c.mlp_k > 0 ? c.mlp_k : Fl;
+    blk->midx = (int32_t*)blk->alloc(4 * B * C * mk);
+    blk->mcnt = (int32_t*)blk->alloc(4 * B * C);
+    for (void* p : blk->allocs)
+        if (!p) return fail(set_error(CSD_ERR_CUDA, "block allocation failed"));
+    *out = blk;
+    return CSD_OK;
+}
+
+csd_status csd_block_destroy(csd_block* blk) {
+    cudaDeviceSynchronize();
+    delete blk;
+    return CSD_OK;
+}
+
+csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int dense,
+                          const int32_t* static_idx, const int32_t* static_counts,
+                          int64_t static_k_max, void* stream) {
+    if (!blk) return set_error(CSD_ERR_VALUE, "null block");
+    const auto& c = blk->cfg;
+    csd_ctx* ctx = reinterpret_cast<csd_ctx*>(blk->ctx);
+    const csd_mode md = blk->mode;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!dense && (!blk->attn_init || !blk->mlp_init))
+        return set_error(CSD_ERR_STATE, "sparse attention step requested before any dense step");
+    const int64_t B = c.batch, N = c.seq, D = c.dim, E = c.head_dim, Hl = c.heads_local;
+    const int64_t Dl = Hl * E, Fl = c.f_local, C = N / c.chunk;
+    const int64_t ak = blk->a_kmax;
+    const int64_t mk = c.mlp_k > 0 ? c.mlp_k : Fl;
+    // ---- attention branch
+    CSD_TRY(csd_project(ctx, md, x_in, blk->wq, B, N, D, Dl, blk->q, stream));
+    CSD_TRY(csd_project(ctx, md, x_in, blk->wk, B, N, D, Dl, blk->k, stream));
+    CSD_TRY(csd_project(ctx, md, x_in, blk->wv, B, N, D, Dl, blk->v, stream));
+    if (dense) {
+        const int nxt = blk->attn_init ? 1 - blk->cur : blk->cur;
+        const float* pm = blk->attn_init ? blk->m[blk->cur] : nullptr;
+        const float* pl = blk->attn_init ? blk->l[blk->cur] : nullptr;
+        CSD_TRY(csd_column_sum_attention(ctx, md, CSD_LAYOUT_BNHE, blk->q, blk->k, blk->v, pm, pl, B,
+                                         Hl, N, E, c.chunk, blk->attn, blk->m[nxt], blk->l[nxt],
+                                         blk->colsum, stream));
+        blk->cur = nxt;
+        const int32_t* ui = blk->aidx;
+        const int32_t* uc = blk->acnt;
+        int64_t ukm = ak;
+        if (static_idx) {
+            ui = static_idx;
+            uc = static_counts;
+            ukm = static_k_max;
+        } else {
+            CSD_TRY(csd_select_top_k(ctx, blk->colsum, B * Hl * C, N, ak, blk->aidx, blk->acnt,
+                                     stream));
+        }
+        if (static_idx) {  // keep a private copy (the cache owns its indices)
+            if (static_k_max != blk->a_kmax) {
+                return set_error(CSD_ERR_SHAPE, "static pattern k_max %lld != block attn_k %lld",
+                                 (long long)static_k_max, (long long)blk->a_kmax);
+            }
+            CSD_CU(cudaMemcpyAsync(blk->aidx, static_idx, 4 * B * Hl * C * ukm,
+                                   cudaMemcpyDeviceToDevice, s), "copy");
+            CSD_CU(cudaMemcpyAsync(blk->acnt, static_counts, 4 * B * Hl * C,
+                                   cudaMemcpyDeviceToDevice, s), "copy");
+        }
+        (void)ui;
+        (void)uc;
+        CSD_TRY(csd_sparse_delta_attention(ctx, md, CSD_LAYOUT_BNHE, blk->q, blk->k, blk->v,
+                                           blk->aidx, blk->acnt, ukm, c.chunk, blk->attn, -1.0f,
+                                           B, Hl, N, E, blk->resid, stream));
+        blk->attn_init = true;
+        blk->attn_age = 0;
+    } else {
+        CSD_TRY(csd_sparse_delta_attention(ctx, md, CSD_LAYOUT_BNHE, blk->q, blk->k, blk->v,
+                                           blk->aidx, blk->acnt, ak, c.chunk, blk->resid, 1.0f, B,
+                                           Hl, N, E, blk->attn, stream));
+        blk->attn_age += 1;
+    }
+    // x1 = x + O Wo
+    if (md == CSD_MODE_PROD) {
+        CSD_TRY(csd::gemm_bf16(blk->ctx, blk->attn, blk->wo, false, blk->proj, true, B * N, D, Dl,
+                               0.0f, s));
+        CSD_CU(prod_add_bf16_f32(x_in, blk->proj, B * N * D, blk->x_mid, s), "add");
+        blk->ctx->launches += 1;
+    } else {
+        CSD_TRY(csd_project(ctx, md, blk->attn, blk->wo, B, N, Dl, D, blk->proj, stream));
+        CSD_TRY(csd_add(ctx, md, x_in, blk->proj, B * N * D, blk->x_mid, stream));
+    }
+    // ---- MLP branch
+    if (dense) {
+        CSD_TRY(csd_dense_mlp(ctx, md, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B, N, D, Fl,
+                              c.chunk, blk->mout, blk->act, stream));
+        CSD_TRY(csd_mlp_tile_means(ctx, md, blk->x_mid, blk->w1, B, N, D, Fl, c.chunk, blk->tmeans,
+                                   stream));
+        blk->mlp_init = true;
+        blk->mlp_age = 0;
+    } else {
+        CSD_TRY(csd_mlp_change_indices(ctx, md, blk->x_mid, blk->w1, blk->tmeans, B, N, D, Fl, mk,
+                                       c.chunk, blk->midx, blk->mcnt, stream));
+        CSD_TRY(csd_sparse_delta_mlp(ctx, md, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->midx,
+                                     blk->mcnt, mk, c.chunk, B, N, D, Fl, blk->act, blk->mout,
+                                     stream));
+        blk->mlp_age += 1;
+    }
+    if (md == CSD_MODE_PROD) {
+        CSD_CU(prod_add_bf16_f32(blk->x_mid, blk->mout, B * N * D, x_out, s), "add");
+        blk->ctx->launches += 1;
+    } else {
+        CSD_TRY(csd_add(ctx, md, blk->x_mid, blk->mout, B * N * D, x_out, stream));
+    }
+    return CSD_OK;
+}
+
+csd_status csd_block_cache(csd_block* blk, int which, void* out, int32_t* counts_out,
+                           void* stream) {
+    if (!blk) return set_error(CSD_ERR_VALUE, "null block");
+    const auto& c = blk->cfg;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t B = c.batch, N = c.seq, D = c.dim, E = c.head_dim, Hl = c.heads_local;
+    const int64_t Fl = c.f_local, C = N / c.chunk;
+    csd_ctx* ctx = reinterpret_cast<csd_ctx*>(blk->ctx);
+    switch (which) {
+        case 0: {  // residual [B,H,N,E] fp32 from token-major storage
+            std::vector<char> dummy;
+            const size_t es = esz(blk->mode);
+            for (int64_t b = 0; b < B; ++b)
+                for (int64_t h = 0; h < Hl; ++h) {
+                    // strided 2D copy: N rows of E elements, src pitch Hl*E
+                    const char* src = (const char*)blk->resid + ((b * N) * Hl + h) * E * es;
+                    float* dst = (float*)out + ((b * Hl + h) * N) * E;
+                    if (blk->mode == CSD_MODE_PROD) {
+                        float* tmp = (float*)blk->ctx->ws(csd::kWsPre, 4 * N * Hl * E);
+                        CSD_CU(prod_cast_bf16_f32((const char*)blk->resid + b * N * Hl * E * es, tmp,
+                                                  N * Hl * E, s), "cast");
+                        CSD_CU(cudaMemcpy2DAsync(dst, E * 4, tmp + h * E, Hl * E * 4, E * 4, N,
+                                                 cudaMemcpyDeviceToDevice, s), "copy");
+                    } else {
+                        CSD_CU(cudaMemcpy2DAsync(dst, E * 4, src, Hl * E * 4, E * 4, N,
+                                                 cudaMemcpyDeviceToDevice, s), "copy");
+                    }
+                }
+            return CSD_OK;
+        }
+        case 1:
+            CSD_CU(cudaMemcpyAsync(out, blk->m[blk->cur], 4 * B * Hl * N, cudaMemcpyDeviceToDevice, s), "copy");
+            return CSD_OK;
+        case 2:
+            CSD_CU(cudaMemcpyAsync(out, blk->l[blk->cur], 4 * B * Hl * N, cudaMemcpyDeviceToDevice, s), "copy");
+            return CSD_OK;
+        case 3:
+            return csd_mlp_act_cache_to_ref(ctx, blk->mode, blk->act, B, N, Fl, c.chunk, (float*)out,
+                                            stream);
+        case 4:
+            CSD_CU(cudaMemcpyAsync(out, blk->mout, 4 * B * N * D, cudaMemcpyDeviceToDevice, s), "copy");
+            return CSD_OK;
+        case 5:
+            CSD_CU(cudaMemcpyAsync(out, blk->tmeans, 4 * B * C * Fl, cudaMemcpyDeviceToDevice, s), "copy");
+            return CSD_OK;
+        case 6:
+            CSD_CU(cudaMemcpyAsync(out, blk->aidx, 4 * B * Hl * C * blk->a_kmax, cudaMemcpyDeviceToDevice, s), "copy");
+            if (counts_out)
+                CSD_CU(cudaMemcpyAsync(counts_out, blk->acnt, 4 * B * Hl * C, cudaMemcpyDeviceToDevice, s), "copy");
+            return CSD_OK;
+        case 7: {
+            const int64_t mk = c.mlp_k > 0 ? c.mlp_k : Fl;
+            CSD_CU(cudaMemcpyAsync(out, blk->midx, 4 * B * C * mk, cudaMemcpyDeviceToDevice, s), "copy");
+            if (counts_out)
+                CSD_CU(cudaMemcpyAsync(counts_out, blk->mcnt, 4 * B * C, cudaMemcpyDeviceToDevice, s), "copy");
+            return CSD_OK;
+        }
+    }
+    (void)E;
+    return set_error(CSD_ERR_VALUE, "unknown cache view %d", which);
+}
+
+}  // extern "C"

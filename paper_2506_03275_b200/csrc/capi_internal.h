@@ -1,0 +1,51 @@
+// capi_internal.h — host-side context shared by the C-ABI translation units.
+#pragma once
+
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <utility>
+#include <vector>
+
+#include "csd_b200.h"
+#include "kernels.h"
+
+namespace csd {
+
+enum WsSlot {
+    kWsTopk = 0,
+    kWsLogits,
+    kWsProbs,
+    kWsStatsM,
+    kWsStatsL,
+    kWsMeans,
+    kWsScores,
+    kWsDelta,
+    kWsPre,
+    kWsAct,
+    kWsIdx,
+    kWsCounts,
+    kWsCount
+};
+
+struct Ctx {
+    int device = 0;
+    int sm_count = 0;
+    uint32_t* flags = nullptr;  // device error bits (kFlag*)
+    cublasHandle_t cublas = nullptr;
+    std::vector<std::pair<void*, size_t>> bufs;
+    int64_t launches = 0;          // our kernels launched through this context
+    int64_t library_launches = 0;  // cuBLAS GEMM calls
+    bool validate_prod = true;     // PROD-mode async index validation
+
+    void* ws(int slot, size_t bytes);
+    cublasHandle_t blas();
+};
+
+csd_status set_error(csd_status s, const char* fmt, ...);
+csd_status cuda_status(cudaError_t e, const char* where);
+csd_status check_flags(Ctx* ctx, cudaStream_t s);
+csd_status gemm_bf16(Ctx* ctx, const void* a, const void* b, bool b_nk, void* c, bool c_f32,
+                     int64_t m, int64_t n, int64_t k, float beta, cudaStream_t s);
+
+}  // namespace csd

@@ -1,0 +1,113 @@
+// kernels.h — internal launcher declarations (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace csd {
+namespace dev {
+
+// Device-side error flags (checked by csd_ctx_sync).  Kernels that validate
+// data set a bit and keep going; the host maps the first bit to a status.
+enum : uint32_t {
+    kFlagIndexRange = 1u << 0,
+    kFlagIndexDup = 1u << 1,
+    kFlagNonFinite = 1u << 2,
+    kFlagCountRange = 1u << 3,
+};
+
+// ---- check mode (check_kernels.cu) ----------------------------------------
+cudaError_t check_attention_logits(const float* q, const float* k, int layout, int64_t batch,
+                                   int64_t heads, int64_t n, int64_t e, int64_t chunk,
+                                   const int32_t* idx, const int32_t* counts, int64_t k_max,
+                                   float* logits, cudaStream_t s);
+cudaError_t check_softmax(float* buf, int64_t rows, int64_t rows_per_batch, int64_t stride,
+                          const int32_t* counts, int64_t full, float* row_max, float* exp_sum,
+                          uint32_t* flags, cudaStream_t s);
+cudaError_t check_attention_pv(const float* probs, const float* v, int layout, int64_t batch,
+                               int64_t heads, int64_t n, int64_t e, int64_t chunk,
+                               const int32_t* idx, const int32_t* counts, int64_t k_max,
+                               const float* base, float scale, float* out, cudaStream_t s);
+cudaError_t check_colsum(const float* logits, const float* m, const float* l, int64_t bh_count,
+                         int64_t n, int64_t chunk, float* out, cudaStream_t s);
+cudaError_t check_project(const float* x, const float* w, int64_t batch, int64_t n, int64_t d,
+                          int64_t dout, float* out, cudaStream_t s);
+cudaError_t check_add(const float* a, const float* b, int64_t numel, float* out, cudaStream_t s);
+cudaError_t check_dense_mlp(const float* x, const float* w1, const float* b1, const float* w2,
+                            const float* b2, int64_t batch, int64_t n, int64_t d, int64_t f,
+                            float* act_ref, float* out, cudaStream_t s);
+cudaError_t check_tile_means(const float* x, const float* w1, int64_t batch, int64_t n, int64_t d,
+                             int64_t f, int64_t chunk, float* means_ws, float* out,
+                             cudaStream_t s);
+cudaError_t check_absdiff(const float* a, const float* b, int64_t numel, float* out,
+                          cudaStream_t s);
+cudaError_t check_sparse_delta_mlp(const float* x, const float* w1, const float* b1,
+                                   const float* w2, const int32_t* idx, const int32_t* counts,
+                                   int64_t k_max, int64_t chunk, int64_t batch, int64_t n,
+                                   int64_t d, int64_t f, float* act_ref, float* out_cache,
+                                   float* ws, cudaStream_t s);
+
+// ---- shared (both modes) ---------------------------------------------------
+// topk.cu
+cudaError_t topk_rows(const float* scores, int64_t rows, int64_t m, int64_t k, int32_t* idx,
+                      int32_t* counts, cudaStream_t s);
+int64_t topk_max_k();
+cudaError_t topk_rows_global(const float* scores, int64_t rows, int64_t m, int64_t k,
+                             int32_t* idx, int32_t* counts, uint64_t* ws, cudaStream_t s);
+cudaError_t validate_index_set(const int32_t* idx, const int32_t* counts, int64_t rows,
+                               int64_t k_max, int64_t domain, uint32_t* flags, cudaStream_t s);
+// voxel.cu
+cudaError_t voxel_reorder(const void* src, void* dst, int64_t batch, int64_t t, int64_t h,
+                          int64_t w, int64_t vt, int64_t vh, int64_t vw, int64_t row_bytes,
+                          int inverse, cudaStream_t s);
+
+// ---- production (prod_kernels.cu / attn_tc.cu) -----------------------------
+struct AttnTcArgs {
+    const void* q;  // bf16
+    const void* k;
+    const void* v;
+    const int32_t* idx;     // nullable = dense (all keys, contiguous TMA tiles)
+    const int32_t* counts;  // per (b,h,chunk)
+    int64_t k_max;
+    const void* base;  // bf16, nullable
+    float scale;       // out = base + scale * O / l   (or O / l without base)
+    void* out;         // bf16
+    float* row_max;    // nullable [B,H,N] (natural-log units, like softmax_rows)
+    float* exp_sum;    // nullable
+    const float* prev_m;  // nullable: colsum stats (fresh if null and colsum requested)
+    const float* prev_l;
+    float* colsum;     // nullable [B,H,N/c,N]
+    int layout;
+    int64_t batch, heads, n, e, chunk;
+};
+// Returns cudaErrorNotSupported for shapes outside the envelope.
+cudaError_t attn_tc(const AttnTcArgs& a, cudaStream_t s);
+bool attn_tc_supported(int64_t e, int64_t chunk);
+
+cudaError_t prod_cast_f32_bf16(const float* in, void* out, int64_t n, cudaStream_t s);
+cudaError_t prod_cast_bf16_f32(const void* in, float* out, int64_t n, cudaStream_t s);
+
+// prod MLP (prod_kernels.cu)
+cudaError_t prod_tile_means(const void* x, const void* w1, int64_t batch, int64_t n, int64_t d,
+                            int64_t f, int64_t chunk, float* means_ws, float* out,
+                            cudaStream_t s);
+cudaError_t prod_bias_gelu(const float* pre, const float* b1, int64_t rows, int64_t f, void* act,
+                           cudaStream_t s);
+cudaError_t prod_bias_add_rows(float* out, const float* b2, int64_t rows, int64_t d,
+                               cudaStream_t s);
+cudaError_t prod_act_to_cm(const void* act, int64_t batch, int64_t n, int64_t f, int64_t chunk,
+                           void* cm, cudaStream_t s);
+// residual adds for the block runner: out_bf16 = a_bf16 + b_f32
+cudaError_t prod_add_bf16_f32(const void* a, const float* b, int64_t numel, void* out,
+                              cudaStream_t s);cudaError_t prod_sparse_delta_mlp(const void* x, const void* w1, const float* b1, const void* w2,
+                                  const int32_t* idx, const int32_t* counts, int64_t k_max,
+                                  int64_t chunk, int64_t batch, int64_t n, int64_t d, int64_t f,
+                                  void* act_cm, float* out_cache, void* delta_ws,
+                                  cudaStream_t s);
+cudaError_t prod_act_cm_to_ref(const void* act_cm, int64_t batch, int64_t n, int64_t f,
+                               int64_t chunk, float* out, cudaStream_t s);
+cudaError_t prod_absdiff(const float* a, const float* b, int64_t numel, float* out,
+                         cudaStream_t s);
+
+}  // namespace dev
+}  // namespace csd
