@@ -133,19 +133,37 @@ def run_ours(args, rank, world):
                          attn_k=attn_k, mlp_k=mlp_k)
     blk = ops.Block(bc, make_weights(cfg), production=True)
     ctx = ops.context()
-    ctx_launch0 = ctx.launches
-    stream = torch.cuda.current_stream()
     gen = torch.Generator(device="cuda").manual_seed(1235 + rank)
     x = torch.randn((1, n, cfg["dim"]), device="cuda", generator=gen).to(torch.bfloat16)
     y = torch.empty_like(x)
     period = args.dense_interval + 1
 
-    def step(s, xin, yout):
-        blk.step(xin, dense=(s % period == 0), out=yout)
+    # warm-up (eager, on a side stream as graph capture requires): the first step is the
+    # mandatory dense refresh (schedule.cpp:70-74), then sparse steps
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for s in range(args.warmup):
+            blk.step(x, dense=(s % period == 0), out=y)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    # one CUDA graph per step kind (the block's host control flow is static per kind)
+    l_cap = ctx.launches
+    g_dense, g_sparse = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_dense):
+        blk.step(x, dense=True, out=y)
+    launches_dense = ctx.launches - l_cap
+    l_cap = ctx.launches
+    with torch.cuda.graph(g_sparse):
+        blk.step(x, dense=False, out=y)
+    launches_sparse = ctx.launches - l_cap
+    torch.cuda.synchronize()
 
-    # warm-up: starts with the mandatory dense step (schedule.cpp:70-74)
-    for s in range(args.warmup):
-        step(s, x, y)
+    def step(s):
+        (g_dense if s % period == 0 else g_sparse).replay()
+
+    for s in range(2 * period):  # graph warm-up
+        step(s)
     torch.cuda.synchronize()
 
     def barrier():
@@ -160,42 +178,40 @@ def run_ours(args, rank, world):
         return float(t.item())
 
     # ---- timed region: K schedule steps, starting at a dense refresh
-    l0 = ctx.launches
-    lib0 = None
     barrier()
     torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    per_step = []
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(torch.cuda.current_device()) as clk:
         ev0.record(stream)
-        marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
         marks[0].record(stream)
         for s in range(args.steps):
-            step(s, x, y)
+            step(s)
             marks[s + 1].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
     total_ms = max_over_ranks(ev0.elapsed_time(ev1))
-    launches = ctx.launches - l0
+    launches = sum(launches_dense if s % period == 0 else launches_sparse
+                   for s in range(args.steps))
     step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
     dense_ms = [t for i, t in enumerate(step_ms) if i % period == 0]
     sparse_ms = [t for i, t in enumerate(step_ms) if i % period != 0]
     ms_per_step = total_ms / args.steps
     clocks = clk.summary()
 
-    # ---- e2e: host buffers through the public API (H2D of x, D2H of the output each step)
+    # ---- e2e: host buffers each step (H2D of x from pinned memory, D2H of the output)
     xh = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
     xh.copy_(x.cpu())
     yh = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
-    xd = torch.empty_like(x)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for s in range(args.steps):
-        xd.copy_(xh, non_blocking=True)
-        step(s, xd, y)
+        x.copy_(xh, non_blocking=True)
+        step(s)
         yh.copy_(y, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -269,20 +285,32 @@ def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
 
-    def timed(fn):
-        ts = []
-        for i in range(reps + 3):
-            flush.fill_(float(i))
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
+    def graph_of(fn):
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
             fn()
-            b.record(stream)
-            torch.cuda.synchronize()
-            if i >= 3:
-                ts.append(a.elapsed_time(b))
-        return statistics.median(ts)
+        stream.wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return g
 
+    def timed(fn):
+        g = graph_of(fn)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(reps + 3)]
+        for i, (a, b) in enumerate(evs):
+            flush.fill_(float(i))  # evict L2 (256 MB write) between repetitions
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+        torch.cuda.synchronize()
+        return statistics.median(a.elapsed_time(b) for a, b in evs[3:])
+
+    ops.context().set_validation(False)  # the index set comes from top-k: valid by construction
     t_sparse = timed(lambda: ops.sparse_delta_attention(q, k, v, idx, base, 1.0, layout=1, out=out))
+    ops.context().set_validation(True)
     t_dense = timed(lambda: ops.dense_attention(q, k, v, layout=1))
     elem = 2
     alg_bytes = 5 * n * h * e * elem  # Q, K, V, base, out

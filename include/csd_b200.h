@@ -70,6 +70,9 @@ csd_status csd_ctx_destroy(csd_ctx* ctx);
 /* Synchronises `stream` and surfaces in-kernel validation failures
  * (duplicate / out-of-range ids, non-finite logits) as the matching status. */
 csd_status csd_ctx_sync(csd_ctx* ctx, void* stream);
+/* PROD-mode index-set validation on every sparse call (default on; the block
+ * runner disables it for its own top-k sets, which are valid by construction). */
+csd_status csd_ctx_set_validation(csd_ctx* ctx, int enabled);
 /* Number of kernels this context launched since creation (instrumentation). */
 int64_t csd_ctx_launch_count(const csd_ctx* ctx);
 

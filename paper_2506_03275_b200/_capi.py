@@ -41,6 +41,7 @@ SIGNATURES = {
     "csd_ctx_destroy": (i32, [p]),
     "csd_ctx_sync": (i32, [p, p]),
     "csd_ctx_launch_count": (i64, [p]),
+    "csd_ctx_set_validation": (i32, [p, C.c_int]),
     "csd_voxel_permutation": (i32, [i64] * 6 + [p]),
     "csd_voxel_reorder": (i32, [p, fp, fp] + [i64] * 8 + [C.c_int, p]),
     "csd_select_top_k": (i32, [p, fp, i64, i64, i64, fp, fp, p]),

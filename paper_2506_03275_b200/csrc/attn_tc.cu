@@ -480,9 +480,13 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
     p.chunks = (int)(a.n / a.chunk);
     p.qk_scale_log2 = kLog2e / std::sqrt((float)E);
     auto kern = k_attn_tc<E, NT>;
-    cudaError_t err =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
-    if (err != cudaSuccess) return err;
+    static bool attr_done = false;  // once per instantiation (keeps graph capture clean)
+    if (!attr_done) {
+        cudaError_t err =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
+        if (err != cudaSuccess) return err;
+        attr_done = true;
+    }
     const unsigned grid = (unsigned)(a.batch * a.heads * p.chunks);
     kern<<<grid, L::kThreads, L::kSmemAlloc, s>>>(tq, tk, tv, tkg, tvg, p);
     return cudaGetLastError();

@@ -199,8 +199,19 @@ csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int den
     CSD_TRY(csd_project(ctx, md, x_in, blk->wq, B, N, D, Dl, blk->q, stream));
     CSD_TRY(csd_project(ctx, md, x_in, blk->wk, B, N, D, Dl, blk->k, stream));
     CSD_TRY(csd_project(ctx, md, x_in, blk->wv, B, N, D, Dl, blk->v, stream));
+    // Index sets produced inside the block are valid by construction (top-k);
+    // static patterns were validated when supplied.  Skip per-call validation.
+    struct ValidateGuard {
+        Ctx* c;
+        bool old;
+        ~ValidateGuard() { c->validate_prod = old; }
+    } vguard{blk->ctx, blk->ctx->validate_prod};
+    blk->ctx->validate_prod = false;
     if (dense) {
-        const int nxt = blk->attn_init ? 1 - blk->cur : blk->cur;
+        // PROD reads the stale stats and writes the fresh ones row-by-row in the
+        // same thread, so one buffer suffices (and the step stays graph-capturable);
+        // CHECK mode's colsum pass re-reads the stats after softmax -> double buffer.
+        const int nxt = (blk->attn_init && md == CSD_MODE_CHECK) ? 1 - blk->cur : blk->cur;
         const float* pm = blk->attn_init ? blk->m[blk->cur] : nullptr;
         const float* pl = blk->attn_init ? blk->l[blk->cur] : nullptr;
         CSD_TRY(csd_column_sum_attention(ctx, md, CSD_LAYOUT_BNHE, blk->q, blk->k, blk->v, pm, pl, B,

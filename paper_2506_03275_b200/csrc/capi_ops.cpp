@@ -74,6 +74,11 @@ csd_status prod_attn(Ctx* c, const AttnTcArgs& a, cudaStream_t s) {
 
 extern "C" {
 
+csd_status csd_ctx_set_validation(csd_ctx* ctx, int enabled) {
+    reinterpret_cast<Ctx*>(ctx)->validate_prod = enabled != 0;
+    return CSD_OK;
+}
+
 // ---------------------------------------------------------------- attention
 csd_status csd_dense_attention(csd_ctx* ctx, csd_mode mode, csd_layout layout, const void* q,
                                const void* k, const void* v, int64_t batch, int64_t heads,
@@ -296,10 +301,15 @@ csd_status csd_sparse_delta_mlp(csd_ctx* ctx, csd_mode mode, const void* x, cons
             CSD_CU(validate_index_set(idx, counts, rows, k_max, f, c->flags, s), "validate");
             c->launches += 1;
         }
-        void* dws = c->ws(csd::kWsDelta, 2 * rows * chunk * (k_max ? k_max : 1));
+        if (!mlp_tc_supported(d, chunk))
+            return set_error(CSD_ERR_UNSUPPORTED,
+                             "production sparse-delta MLP needs model_dim %% 128 == 0 and chunk <= 256 "
+                             "(got D=%lld, chunk=%lld)", (long long)d, (long long)chunk);
+        const int64_t k_pad = (k_max + 127) / 128 * 128;
+        void* dws = c->ws(csd::kWsDelta, 2 * rows * chunk * (k_pad ? k_pad : 128));
         CSD_TRY(need_ws(dws));
-        CSD_CU(prod_sparse_delta_mlp(x, w1, b1, w2, idx, counts, k_max, chunk, batch, n, d, f,
-                                     act_cache, out_cache, dws, s), "sparse_delta_mlp");
+        CSD_CU(prod_sparse_delta_mlp_tc(x, w1, b1, w2, idx, counts, k_max, chunk, batch, n, d, f,
+                                        act_cache, out_cache, dws, s), "sparse_delta_mlp");
         c->launches += 2;
         return CSD_OK;
     }

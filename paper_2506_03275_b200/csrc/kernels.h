@@ -99,11 +99,13 @@ cudaError_t prod_act_to_cm(const void* act, int64_t batch, int64_t n, int64_t f,
                            void* cm, cudaStream_t s);
 // residual adds for the block runner: out_bf16 = a_bf16 + b_f32
 cudaError_t prod_add_bf16_f32(const void* a, const float* b, int64_t numel, void* out,
-                              cudaStream_t s);cudaError_t prod_sparse_delta_mlp(const void* x, const void* w1, const float* b1, const void* w2,
-                                  const int32_t* idx, const int32_t* counts, int64_t k_max,
-                                  int64_t chunk, int64_t batch, int64_t n, int64_t d, int64_t f,
-                                  void* act_cm, float* out_cache, void* delta_ws,
-                                  cudaStream_t s);
+                              cudaStream_t s);// mlp_tc.cu: delta_ws >= B*C*chunk*round_up(k_max,128) bf16
+bool mlp_tc_supported(int64_t d, int64_t chunk);
+cudaError_t prod_sparse_delta_mlp_tc(const void* x, const void* w1, const float* b1,
+                                     const void* w2, const int32_t* idx, const int32_t* counts,
+                                     int64_t k_max, int64_t chunk, int64_t batch, int64_t n,
+                                     int64_t d, int64_t f, void* act_cm, float* out_cache,
+                                     void* delta_ws, cudaStream_t s);
 cudaError_t prod_act_cm_to_ref(const void* act_cm, int64_t batch, int64_t n, int64_t f,
                                int64_t chunk, float* out, cudaStream_t s);
 cudaError_t prod_absdiff(const float* a, const float* b, int64_t numel, float* out,

@@ -1,18 +1,9 @@
 // prod_kernels.cu — CSD_MODE_PROD MLP-side kernels (bf16 storage, fp32 math).
 //
-//   tile means  (mlp.cpp:83-96):  chunk means of x, then T = means @ W1^T
-//   sparse-delta MLP (mlp.cpp:120-182), one-pass:
-//       GEMM1  a = gelu(x_c W1[S]^T + b1[S])      per chunk c, gathered W1 rows
-//       delta  = a - A_cache[c, S, :]; A_cache[c, S, :] = a   (chunk-major cache)
-//       GEMM2  M_cache[c rows] += delta W2[S]      gathered W2 rows
-//   The activation cache uses the chunk-major layout [B, C, F, chunk] so the
-//   GEMM1 epilogue's cache read-modify-write is contiguous along the chunk's
-//   rows for each selected neuron (reference layout [B,N,F] would scatter 2 B
-//   accesses F apart).
-//
-// These are tiled CUDA-core kernels (64x64 output tiles, 4x4 per thread,
-// fp32 FMA) — the functional production baseline.  The dense MLP uses cuBLAS
-// (plain library GEMM) from capi.cpp.
+//   tile means (mlp.cpp:83-96): chunk means of x, then T = means @ W1^T
+//   casts, |delta| scores, bias/GELU epilogue of the dense (cuBLAS) MLP, and the
+//   activation-cache layout conversions (reference [B,N,F] <-> chunk-major
+//   [B,C,F,chunk] used by the tcgen05 sparse-delta MLP in mlp_tc.cu).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -66,140 +57,6 @@ __global__ void k_chunk_mean_bf16(const __nv_bfloat16* x, int64_t n, int64_t d, 
 }
 
 constexpr int GT = 64, GK = 32;
-
-// Sparse MLP GEMM1 + refresh: grid (k_max/64, chunk/64 up, B*C)
-__global__ void __launch_bounds__(256)
-k_smlp_gemm1(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w1,
-             const float* __restrict__ b1, const int32_t* __restrict__ idx,
-             const int32_t* __restrict__ counts, int64_t k_max, int64_t chunk, int64_t n,
-             int64_t d, int64_t f, __nv_bfloat16* __restrict__ act_cm,
-             __nv_bfloat16* __restrict__ delta_ws) {
-    __shared__ float As[GK][GT + 1];
-    __shared__ float Bs[GK][GT + 1];
-    __shared__ int32_t sidx[GT];
-    const int64_t z = blockIdx.z;
-    const int64_t cnt = counts[z];
-    const int64_t n0 = (int64_t)blockIdx.x * GT, m0 = (int64_t)blockIdx.y * GT;
-    if (n0 >= cnt || m0 >= chunk) return;
-    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-    const int64_t nc = n / chunk;
-    const int64_t b = z / nc, c = z % nc;
-    const __nv_bfloat16* xa = x + (b * n + c * chunk) * d;
-    const int32_t* ids = idx + z * k_max;
-    if (tid < GT) sidx[tid] = (n0 + tid < cnt) ? ids[n0 + tid] : ids[0];
-    __syncthreads();
-    float acc[4][4] = {};
-    for (int64_t k0 = 0; k0 < d; k0 += GK) {
-        for (int i = tid; i < GT * GK; i += 256) {
-            const int r = i / GK, kk = i % GK;
-            const int64_t gm = m0 + r, gk = k0 + kk;
-            As[kk][r] = (gm < chunk && gk < d) ? __bfloat162float(xa[gm * d + gk]) : 0.f;
-            Bs[kk][r] = (gk < d) ? __bfloat162float(w1[(int64_t)sidx[r] * d + gk]) : 0.f;
-        }
-        __syncthreads();
-#pragma unroll 8
-        for (int kk = 0; kk < GK; ++kk) {
-            float av[4], bv[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { av[i] = As[kk][ty * 4 + i]; bv[i] = Bs[kk][tx * 4 + i]; }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj) acc[i][jj] += av[i] * bv[jj];
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int64_t r = m0 + ty * 4 + i;
-        if (r >= chunk) continue;
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-            const int64_t col = n0 + tx * 4 + jj;
-            if (col >= cnt) continue;
-            const int32_t neuron = sidx[tx * 4 + jj];
-            const float a = fast_gelu(acc[i][jj] + b1[neuron]);
-            __nv_bfloat16* cache = act_cm + ((z * f + neuron) * chunk + r);
-            const float old = __bfloat162float(*cache);
-            const __nv_bfloat16 a16 = __float2bfloat16_rn(a);
-            *cache = a16;
-            delta_ws[(z * chunk + r) * k_max + col] = __float2bfloat16_rn(__bfloat162float(a16) - old);
-        }
-    }
-}
-
-// Sparse MLP GEMM2: out_cache[z rows, :] += delta[z] @ W2[S]; grid (D/64, chunk/64, B*C)
-__global__ void __launch_bounds__(256)
-k_smlp_gemm2(const __nv_bfloat16* __restrict__ delta_ws, const __nv_bfloat16* __restrict__ w2,
-             const int32_t* __restrict__ idx, const int32_t* __restrict__ counts, int64_t k_max,
-             int64_t chunk, int64_t n, int64_t d, float* __restrict__ out_cache) {
-    __shared__ float As[GK][GT + 1];
-    __shared__ float Bs[GK][GT + 1];
-    const int64_t z = blockIdx.z;
-    const int64_t cnt = counts[z];
-    const int64_t n0 = (int64_t)blockIdx.x * GT, m0 = (int64_t)blockIdx.y * GT;
-    if (cnt == 0 || m0 >= chunk || n0 >= d) return;
-    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-    const int64_t nc = n / chunk;
-    const int64_t b = z / nc, c = z % nc;
-    const __nv_bfloat16* da = delta_ws + z * chunk * k_max;
-    const int32_t* ids = idx + z * k_max;
-    float acc[4][4] = {};
-    for (int64_t k0 = 0; k0 < cnt; k0 += GK) {
-        for (int i = tid; i < GT * GK; i += 256) {
-            const int r = i / GK, kk = i % GK;
-            const int64_t gm = m0 + r, gk = k0 + kk;
-            As[kk][r] = (gm < chunk && gk < cnt) ? __bfloat162float(da[gm * k_max + gk]) : 0.f;
-        }
-        for (int i = tid; i < GT * GK; i += 256) {
-            const int kk = i / GT, col = i % GT;
-            const int64_t gk = k0 + kk, gn = n0 + col;
-            Bs[kk][col] = (gk < cnt && gn < d) ? __bfloat162float(w2[(int64_t)ids[gk] * d + gn]) : 0.f;
-        }
-        __syncthreads();
-#pragma unroll 8
-        for (int kk = 0; kk < GK; ++kk) {
-            float av[4], bv[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { av[i] = As[kk][ty * 4 + i]; bv[i] = Bs[kk][tx * 4 + i]; }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj) acc[i][jj] += av[i] * bv[jj];
-        }
-        __syncthreads();
-    }
-    float* o = out_cache + (b * n + c * chunk) * d;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int64_t r = m0 + ty * 4 + i;
-        if (r >= chunk) continue;
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-            const int64_t col = n0 + tx * 4 + jj;
-            if (col < d) o[r * d + col] += acc[i][jj];
-        }
-    }
-}
-
-cudaError_t prod_sparse_delta_mlp(const void* x, const void* w1, const float* b1, const void* w2,
-                                  const int32_t* idx, const int32_t* counts, int64_t k_max,
-                                  int64_t chunk, int64_t batch, int64_t n, int64_t d, int64_t f,
-                                  void* act_cm, float* out_cache, void* delta_ws,
-                                  cudaStream_t s) {
-    const int64_t total = batch * (n / chunk);
-    if (total == 0 || k_max == 0) return cudaSuccess;
-    dim3 g1((unsigned)((k_max + GT - 1) / GT), (unsigned)((chunk + GT - 1) / GT), (unsigned)total);
-    k_smlp_gemm1<<<g1, 256, 0, s>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)w1, b1, idx,
-                                    counts, k_max, chunk, n, d, f, (__nv_bfloat16*)act_cm,
-                                    (__nv_bfloat16*)delta_ws);
-    cudaError_t err = cudaGetLastError();
-    if (err != cudaSuccess) return err;
-    dim3 g2((unsigned)((d + GT - 1) / GT), (unsigned)((chunk + GT - 1) / GT), (unsigned)total);
-    k_smlp_gemm2<<<g2, 256, 0, s>>>((const __nv_bfloat16*)delta_ws, (const __nv_bfloat16*)w2, idx,
-                                    counts, k_max, chunk, n, d, out_cache);
-    return cudaGetLastError();
-}
 
 // T[bc, f] = means[bc, :] . W1[f, :]   grid (F/64, ceil(BC/64))
 __global__ void __launch_bounds__(256)

@@ -64,6 +64,10 @@ class Context:
     def sync(self):
         raise_for(self.lib, self.lib.csd_ctx_sync(self.h, _stream()))
 
+    def set_validation(self, enabled: bool):
+        """PROD-mode per-call index-set validation (CHECK mode always validates)."""
+        raise_for(self.lib, self.lib.csd_ctx_set_validation(self.h, int(bool(enabled))))
+
     @property
     def launches(self) -> int:
         return int(self.lib.csd_ctx_launch_count(self.h))
