@@ -252,17 +252,40 @@ csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int den
                                            Hl, N, E, blk->attn, stream));
         blk->attn_age += 1;
     }
-    // x1 = x + O Wo
     if (md == CSD_MODE_PROD) {
-        CSD_TRY(csd::gemm_bf16(blk->ctx, blk->attn, blk->wo, false, blk->proj, true, B * N, D, Dl,
-                               0.0f, s));
-        CSD_CU(prod_add_bf16_f32(x_in, blk->proj, B * N * D, blk->x_mid, s), "add");
-        blk->ctx->launches += 1;
-    } else {
-        CSD_TRY(csd_project(ctx, md, blk->attn, blk->wo, B, N, Dl, D, blk->proj, stream));
-        CSD_TRY(csd_add(ctx, md, x_in, blk->proj, B * N * D, blk->x_mid, stream));
+        // x1 = x + O Wo: the residual rides in the GEMM (C = x, beta = 1, fp32 accumulate)
+        CSD_CU(cudaMemcpyAsync(blk->x_mid, x_in, 2 * B * N * D, cudaMemcpyDeviceToDevice, s), "copy");
+        CSD_TRY(csd::gemm_bf16(blk->ctx, blk->attn, blk->wo, false, blk->x_mid, false, B * N, D, Dl,
+                               1.0f, s));
+        // ---- MLP branch; x2 = x1 + M is fused into the last MLP kernel's epilogue
+        if (dense) {
+            CSD_TRY(csd::prod_dense_mlp(blk->ctx, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B,
+                                        N, D, Fl, c.chunk, blk->mout, blk->act, blk->x_mid, x_out,
+                                        s));
+            CSD_TRY(csd_mlp_tile_means(ctx, md, blk->x_mid, blk->w1, B, N, D, Fl, c.chunk,
+                                       blk->tmeans, stream));
+            blk->mlp_init = true;
+            blk->mlp_age = 0;
+        } else {
+            CSD_TRY(csd_mlp_change_indices(ctx, md, blk->x_mid, blk->w1, blk->tmeans, B, N, D, Fl,
+                                           mk, c.chunk, blk->midx, blk->mcnt, stream));
+            if (!mlp_tc_supported(D, c.chunk))
+                return set_error(CSD_ERR_UNSUPPORTED, "sparse-delta MLP envelope (D %% 128, chunk <= 256)");
+            const int64_t k_pad = (mk + 127) / 128 * 128;
+            void* dws = blk->ctx->ws(csd::kWsDelta, 2 * B * N * k_pad);
+            if (!dws) return set_error(CSD_ERR_CUDA, "workspace allocation failed");
+            CSD_CU(prod_sparse_delta_mlp_tc(blk->x_mid, blk->w1, blk->b1, blk->w2, blk->midx,
+                                            blk->mcnt, mk, c.chunk, B, N, D, Fl, blk->act,
+                                            blk->mout, dws, s, blk->x_mid, x_out),
+                   "sparse_delta_mlp");
+            blk->ctx->launches += 2;
+            blk->mlp_age += 1;
+        }
+        return CSD_OK;
     }
-    // ---- MLP branch
+    // ---------------- CHECK mode: op for op as model.cpp:200-213
+    CSD_TRY(csd_project(ctx, md, blk->attn, blk->wo, B, N, Dl, D, blk->proj, stream));
+    CSD_TRY(csd_add(ctx, md, x_in, blk->proj, B * N * D, blk->x_mid, stream));
     if (dense) {
         CSD_TRY(csd_dense_mlp(ctx, md, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B, N, D, Fl,
                               c.chunk, blk->mout, blk->act, stream));
@@ -278,12 +301,7 @@ csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int den
                                      stream));
         blk->mlp_age += 1;
     }
-    if (md == CSD_MODE_PROD) {
-        CSD_CU(prod_add_bf16_f32(blk->x_mid, blk->mout, B * N * D, x_out, s), "add");
-        blk->ctx->launches += 1;
-    } else {
-        CSD_TRY(csd_add(ctx, md, blk->x_mid, blk->mout, B * N * D, x_out, stream));
-    }
+    CSD_TRY(csd_add(ctx, md, blk->x_mid, blk->mout, B * N * D, x_out, stream));
     return CSD_OK;
 }
 

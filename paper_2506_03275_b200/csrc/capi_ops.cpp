@@ -72,6 +72,32 @@ csd_status prod_attn(Ctx* c, const AttnTcArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+namespace csd {
+// Dense MLP, PROD (mlp.cpp:49-81): cuBLAS GEMM1 -> bf16 pre; fused bias+GELU writing the
+// row-major activations and the chunk-major cache; cuBLAS GEMM2 -> fp32 M_cache; fused
+// +b2 (and, for the block runner, x_out = x_mid + M_cache).
+csd_status prod_dense_mlp(Ctx* c, const void* x, const void* w1, const float* b1, const void* w2,
+                          const float* b2, int64_t batch, int64_t n, int64_t d, int64_t f,
+                          int64_t chunk, float* out, void* act_cm, const void* x_mid, void* x_out,
+                          cudaStream_t s) {
+    const int64_t rows = batch * n;
+    void* pre = c->ws(kWsPre, 2 * rows * f);
+    void* act = c->ws(kWsAct, 2 * rows * f);
+    CSD_TRY(need_ws(pre));
+    CSD_TRY(need_ws(act));
+    if (!act_cm) {
+        act_cm = c->ws(kWsScores, 2 * rows * f);
+        CSD_TRY(need_ws(act_cm));
+    }
+    CSD_TRY(gemm_bf16(c, x, w1, true, pre, false, rows, f, d, 0.0f, s));
+    CSD_CU(prod_bias_gelu_cm(pre, b1, batch, n, f, chunk, act, act_cm, s), "bias_gelu_cm");
+    CSD_TRY(gemm_bf16(c, act, w2, false, out, true, rows, d, f, 0.0f, s));
+    CSD_CU(prod_bias_add_rows(out, b2, rows, d, x_mid, x_out, s), "bias_add");
+    c->launches += 2;
+    return CSD_OK;
+}
+}  // namespace csd
+
 extern "C" {
 
 csd_status csd_ctx_set_validation(csd_ctx* ctx, int enabled) {
@@ -217,21 +243,9 @@ csd_status csd_dense_mlp(csd_ctx* ctx, csd_mode mode, const void* x, const void*
     const cudaStream_t s = S(stream);
     const int64_t rows = batch * n;
     if (mode == CSD_MODE_PROD) {
-        if (act_out) CSD_TRY(check_chunk(n, chunk, "dense_mlp"));
-        float* pre = (float*)c->ws(csd::kWsPre, sizeof(float) * rows * f);
-        void* act = c->ws(csd::kWsAct, 2 * rows * f);
-        CSD_TRY(need_ws(pre));
-        CSD_TRY(need_ws(act));
-        CSD_TRY(csd::gemm_bf16(c, x, w1, true, pre, true, rows, f, d, 0.0f, s));
-        CSD_CU(prod_bias_gelu(pre, b1, rows, f, act, s), "bias_gelu");
-        CSD_TRY(csd::gemm_bf16(c, act, w2, false, out, true, rows, d, f, 0.0f, s));
-        CSD_CU(prod_bias_add_rows(out, b2, rows, d, s), "bias_add");
-        c->launches += 2;
-        if (act_out) {
-            CSD_CU(prod_act_to_cm(act, batch, n, f, chunk, act_out, s), "act_to_cm");
-            c->launches += 1;
-        }
-        return CSD_OK;
+        CSD_TRY(check_chunk(n, chunk, "dense_mlp"));
+        return csd::prod_dense_mlp(c, x, w1, b1, w2, b2, batch, n, d, f, chunk, out, act_out,
+                                   nullptr, nullptr, s);
     }
     float* act = act_out ? (float*)act_out : (float*)c->ws(csd::kWsAct, sizeof(float) * rows * f);
     CSD_TRY(need_ws(act));
@@ -248,13 +262,19 @@ csd_status csd_mlp_tile_means(csd_ctx* ctx, csd_mode mode, const void* x, const 
     CSD_TRY(check_mlp_shape(batch, n, d, f));
     CSD_TRY(check_chunk(n, chunk, "mlp_tile_means"));
     const cudaStream_t s = S(stream);
+    if (mode == CSD_MODE_PROD) {
+        if (!means_tc_supported(d, f))
+            return set_error(CSD_ERR_UNSUPPORTED, "production tile means need D %% 64 == 0 and F %% 128 == 0");
+        void* ws = c->ws(csd::kWsMeans, prod_means_ws_bytes(batch, n, d, f, chunk));
+        CSD_TRY(need_ws(ws));
+        CSD_CU(prod_tile_means_tc(x, w1, batch, n, d, f, chunk, nullptr, out, ws, s), "tile_means");
+        c->launches += 3;
+        return CSD_OK;
+    }
     float* means = (float*)c->ws(csd::kWsMeans, sizeof(float) * batch * (n / chunk) * d);
     CSD_TRY(need_ws(means));
-    if (mode == CSD_MODE_PROD)
-        CSD_CU(prod_tile_means(x, w1, batch, n, d, f, chunk, means, out, s), "tile_means");
-    else
-        CSD_CU(check_tile_means((const float*)x, (const float*)w1, batch, n, d, f, chunk, means, out,
-                                s), "tile_means");
+    CSD_CU(check_tile_means((const float*)x, (const float*)w1, batch, n, d, f, chunk, means, out, s),
+           "tile_means");
     c->launches += 2;
     return CSD_OK;
 }
@@ -271,16 +291,24 @@ csd_status csd_mlp_change_indices(csd_ctx* ctx, csd_mode mode, const void* x, co
                          (long long)f);
     const cudaStream_t s = S(stream);
     const int64_t rows = batch * (n / chunk);
-    float* fresh = (float*)c->ws(csd::kWsScores, sizeof(float) * rows * f * 2);
-    CSD_TRY(need_ws(fresh));
-    float* delta = fresh + rows * f;
-    CSD_TRY(csd_mlp_tile_means(ctx, mode, x, w1, batch, n, d, f, chunk, fresh, stream));
-    if (mode == CSD_MODE_PROD)
-        CSD_CU(prod_absdiff(fresh, tile_means, rows * f, delta, s), "absdiff");
-    else
-        CSD_CU(check_absdiff(fresh, tile_means, rows * f, delta, s), "absdiff");
-    c->launches += 1;
-    return csd_select_top_k(ctx, delta, rows, f, k, idx, counts, stream);
+    float* scores = (float*)c->ws(csd::kWsScores, sizeof(float) * rows * f * 2);
+    CSD_TRY(need_ws(scores));
+    if (mode == CSD_MODE_PROD) {
+        if (!means_tc_supported(d, f))
+            return set_error(CSD_ERR_UNSUPPORTED, "production tile means need D %% 64 == 0 and F %% 128 == 0");
+        void* ws = c->ws(csd::kWsMeans, prod_means_ws_bytes(batch, n, d, f, chunk));
+        CSD_TRY(need_ws(ws));
+        // |tile_means(x) - T_m| fused into the split-K reduction (mlp.cpp:116)
+        CSD_CU(prod_tile_means_tc(x, w1, batch, n, d, f, chunk, tile_means, scores, ws, s),
+               "tile_means");
+        c->launches += 3;
+    } else {
+        float* fresh = scores + rows * f;
+        CSD_TRY(csd_mlp_tile_means(ctx, mode, x, w1, batch, n, d, f, chunk, fresh, stream));
+        CSD_CU(check_absdiff(fresh, tile_means, rows * f, scores, s), "absdiff");
+        c->launches += 1;
+    }
+    return csd_select_top_k(ctx, scores, rows, f, k, idx, counts, stream);
 }
 
 csd_status csd_sparse_delta_mlp(csd_ctx* ctx, csd_mode mode, const void* x, const void* w1,

@@ -88,15 +88,18 @@ cudaError_t prod_cast_f32_bf16(const float* in, void* out, int64_t n, cudaStream
 cudaError_t prod_cast_bf16_f32(const void* in, float* out, int64_t n, cudaStream_t s);
 
 // prod MLP (prod_kernels.cu)
-cudaError_t prod_tile_means(const void* x, const void* w1, int64_t batch, int64_t n, int64_t d,
-                            int64_t f, int64_t chunk, float* means_ws, float* out,
-                            cudaStream_t s);
-cudaError_t prod_bias_gelu(const float* pre, const float* b1, int64_t rows, int64_t f, void* act,
-                           cudaStream_t s);
+// means_tc.cu: tcgen05 tile means (T, or |T - cached| when cached != null)
+bool means_tc_supported(int64_t d, int64_t f);
+size_t prod_means_ws_bytes(int64_t batch, int64_t n, int64_t d, int64_t f, int64_t chunk);
+cudaError_t prod_tile_means_tc(const void* x, const void* w1, int64_t batch, int64_t n,
+                               int64_t d, int64_t f, int64_t chunk, const float* cached,
+                               float* out, void* ws, cudaStream_t s);
+// dense-step MLP epilogue: act = gelu(pre + b1) row-major + chunk-major cache copy
+cudaError_t prod_bias_gelu_cm(const void* pre, const float* b1, int64_t batch, int64_t n,
+                              int64_t f, int64_t chunk, void* act, void* cm, cudaStream_t s);
+// out += b2 (rows); if x_out: x_out = bf16(x_mid + out)
 cudaError_t prod_bias_add_rows(float* out, const float* b2, int64_t rows, int64_t d,
-                               cudaStream_t s);
-cudaError_t prod_act_to_cm(const void* act, int64_t batch, int64_t n, int64_t f, int64_t chunk,
-                           void* cm, cudaStream_t s);
+                               const void* x_mid, void* x_out, cudaStream_t s);
 // residual adds for the block runner: out_bf16 = a_bf16 + b_f32
 cudaError_t prod_add_bf16_f32(const void* a, const float* b, int64_t numel, void* out,
                               cudaStream_t s);// mlp_tc.cu: delta_ws >= B*C*chunk*round_up(k_max,128) bf16
@@ -105,7 +108,8 @@ cudaError_t prod_sparse_delta_mlp_tc(const void* x, const void* w1, const float*
                                      const void* w2, const int32_t* idx, const int32_t* counts,
                                      int64_t k_max, int64_t chunk, int64_t batch, int64_t n,
                                      int64_t d, int64_t f, void* act_cm, float* out_cache,
-                                     void* delta_ws, cudaStream_t s);
+                                     void* delta_ws, cudaStream_t s,
+                                     const void* x_mid = nullptr, void* x_out = nullptr);
 cudaError_t prod_act_cm_to_ref(const void* act_cm, int64_t batch, int64_t n, int64_t f,
                                int64_t chunk, float* out, cudaStream_t s);
 cudaError_t prod_absdiff(const float* a, const float* b, int64_t numel, float* out,

@@ -36,7 +36,7 @@ struct MlpLayout {
     static constexpr uint32_t kA = 0;                            // [stage][NT] 16 KB
     static constexpr uint32_t kB = kA + kMlpStages * NT * kTile; // [stage] 16 KB
     static constexpr uint32_t kBar = kB + kMlpStages * kTile;
-    static constexpr uint32_t kBytes = kBar + 256;
+    static constexpr uint32_t kBytes = kBar + 128 + 1024;  // barriers + staged ids / biases
     static constexpr uint32_t kSmemAlloc = kBytes + 1024;
     static constexpr uint32_t kThreads = 128 + 128 * NT;
     static constexpr uint32_t kTmemCols = NT * 128 <= 128 ? 128 : 256;
@@ -50,8 +50,33 @@ struct MlpParams {
     __nv_bfloat16* act_cm;
     __nv_bfloat16* delta;
     float* out_cache;
+    const __nv_bfloat16* x_mid;  // optional fused residual: x_out = x_mid + out_cache
+    __nv_bfloat16* x_out;
     int n, chunk, chunks, f, d;
 };
+
+// x_out[row, c0..c0+31] = bf16(x_mid + m) for 32 fp32 values m
+__device__ __forceinline__ void residual32(const MlpParams& p, int64_t row, int col0,
+                                           const float* m) {
+    const uint4* xm = reinterpret_cast<const uint4*>(p.x_mid + row * p.d + col0);
+    uint4* xo = reinterpret_cast<uint4*>(p.x_out + row * p.d + col0);
+    uint4 xv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) xv[q] = xm[q];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint4 v = xv[q];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+        uint4 o;
+        uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float2 f = __bfloat1622float2(h[u]);
+            ow[u] = pack_bf16x2(f.x + m[q * 8 + 2 * u], f.y + m[q * 8 + 2 * u + 1]);
+        }
+        xo[q] = o;
+    }
+}
 
 template <int NT>
 __device__ __forceinline__ void mlp_setup(uint8_t* smem, uint64_t*& full, uint64_t*& empty,
@@ -146,29 +171,43 @@ k_smlp_up(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUte
         const int sw = warp - 4, t = sw >> 2, quad = warp & 3;
         const int r = t * 128 + quad * 32 + lane;  // row within the chunk
         const bool row_ok = r < p.chunk;
+        // stage this tile's neuron ids and biases in smem while the MMAs run, so the
+        // epilogue's cache read-modify-write has no dependent global loads
+        int32_t* s_ids = reinterpret_cast<int32_t*>(smem + L::kBar + 128);
+        float* s_b1 = reinterpret_cast<float*>(smem + L::kBar + 128 + 512);
+        const int et = sw * 32 + lane;
+        if (et < 128) {
+            const int nn = tn * 128 + et;
+            const int neuron = ids[nn < cnt ? nn : cnt - 1];
+            s_ids[et] = neuron;
+            s_b1[et] = p.b1[neuron];
+        }
+        named_bar_sync(1, 128 * NT);
         mbar_wait(done, 0);
         tc_fence_after();
         const uint32_t tacc = tmem + ((uint32_t)(quad * 32) << 16) + t * 128;
         __nv_bfloat16* drow = p.delta + ((int64_t)z * p.chunk + r) * p.k_pad + tn * 128;
+        __nv_bfloat16* __restrict__ cache_base = p.act_cm + (int64_t)z * p.f * p.chunk + r;
 #pragma unroll 1
         for (int cc = 0; cc < 4; ++cc) {
             uint32_t acc[32];
             tmem_ld32(tacc + cc * 32, acc);
             tmem_ld_wait();
             if (!row_ok) continue;
-            float dl[32];
+            const int nvalid = min(32, cnt - (tn * 128 + cc * 32));
+            float old[32], dl[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i)  // all loads first (independent)
+                old[i] = i < nvalid ? __bfloat162float(cache_base[(int64_t)s_ids[cc * 32 + i] * p.chunk])
+                                    : 0.f;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-                const int nn = tn * 128 + cc * 32 + i;
                 dl[i] = 0.f;
-                if (nn < cnt) {
-                    const int neuron = ids[nn];
-                    const float a = fast_gelu(__uint_as_float(acc[i]) + p.b1[neuron]);
+                if (i < nvalid) {
+                    const float a = fast_gelu(__uint_as_float(acc[i]) + s_b1[cc * 32 + i]);
                     const __nv_bfloat16 a16 = __float2bfloat16_rn(a);
-                    __nv_bfloat16* cache = p.act_cm + ((int64_t)z * p.f + neuron) * p.chunk + r;
-                    const float old = __bfloat162float(*cache);
-                    *cache = a16;
-                    dl[i] = __bfloat162float(a16) - old;
+                    cache_base[(int64_t)s_ids[cc * 32 + i] * p.chunk] = a16;
+                    dl[i] = __bfloat162float(a16) - old[i];
                 }
             }
             uint4* dst = reinterpret_cast<uint4*>(drow + cc * 32);
@@ -203,8 +242,22 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int z = blockIdx.y, td = blockIdx.x;
     const int cnt = p.counts[z];
-    if (cnt == 0) return;
     const int b = z / p.chunks, c = z % p.chunks;
+    if (cnt == 0) {  // no recomputed neurons: M_cache unchanged, only the residual
+        if (p.x_out != nullptr) {
+            for (int r = threadIdx.x; r < p.chunk; r += blockDim.x) {
+                const int64_t row = (int64_t)b * p.n + (int64_t)c * p.chunk + r;
+                for (int cc = 0; cc < 4; ++cc) {
+                    float m[32];
+                    const float* src = p.out_cache + row * p.d + td * 128 + cc * 32;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) m[i] = src[i];
+                    residual32(p, row, td * 128 + cc * 32, m);
+                }
+            }
+        }
+        return;
+    }
     const int kblocks = (cnt + 63) / 64;
     const int32_t* ids = p.idx + (int64_t)z * p.k_max;
 
@@ -272,15 +325,22 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta,
             tmem_ld_wait();
             if (!row_ok) continue;
             float4* o4 = reinterpret_cast<float4*>(orow + cc * 32);
+            float m[32];
+            float4 v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = o4[q];  // batch the loads
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                float4 v = o4[q];
-                v.x += __uint_as_float(acc[q * 4 + 0]);
-                v.y += __uint_as_float(acc[q * 4 + 1]);
-                v.z += __uint_as_float(acc[q * 4 + 2]);
-                v.w += __uint_as_float(acc[q * 4 + 3]);
-                o4[q] = v;
+                v[q].x += __uint_as_float(acc[q * 4 + 0]);
+                v[q].y += __uint_as_float(acc[q * 4 + 1]);
+                v[q].z += __uint_as_float(acc[q * 4 + 2]);
+                v[q].w += __uint_as_float(acc[q * 4 + 3]);
+                m[q * 4 + 0] = v[q].x; m[q * 4 + 1] = v[q].y; m[q * 4 + 2] = v[q].z; m[q * 4 + 3] = v[q].w;
             }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o4[q] = v[q];
+            if (p.x_out != nullptr)
+                residual32(p, (int64_t)b * p.n + (int64_t)c * p.chunk + r, td * 128 + cc * 32, m);
         }
     }
     tc_fence_before();
@@ -300,7 +360,7 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
                                const int32_t* idx, const int32_t* counts, int64_t k_max,
                                int64_t chunk, int64_t batch, int64_t n, int64_t d, int64_t f,
                                void* act_cm, float* out_cache, void* delta_ws, int64_t k_pad,
-                               cudaStream_t s) {
+                               cudaStream_t s, const void* x_mid, void* x_out) {
     using L = MlpLayout<NT>;
     const int64_t nc = n / chunk;
     CUtensorMap tx, tw1, tdl, tw2;
@@ -317,6 +377,8 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
     p.act_cm = (__nv_bfloat16*)act_cm;
     p.delta = (__nv_bfloat16*)delta_ws;
     p.out_cache = out_cache;
+    p.x_mid = (const __nv_bfloat16*)x_mid;
+    p.x_out = (__nv_bfloat16*)x_out;
     p.n = (int)n;
     p.chunk = (int)chunk;
     p.chunks = (int)nc;
@@ -342,15 +404,16 @@ cudaError_t prod_sparse_delta_mlp_tc(const void* x, const void* w1, const float*
                                      const void* w2, const int32_t* idx, const int32_t* counts,
                                      int64_t k_max, int64_t chunk, int64_t batch, int64_t n,
                                      int64_t d, int64_t f, void* act_cm, float* out_cache,
-                                     void* delta_ws, cudaStream_t s) {
+                                     void* delta_ws, cudaStream_t s, const void* x_mid,
+                                     void* x_out) {
     if (!mlp_tc_supported(d, chunk)) return cudaErrorNotSupported;
     if (k_max == 0) return cudaSuccess;
     const int64_t k_pad = (k_max + 127) / 128 * 128;
     if (chunk > 128)
         return launch_smlp<2>(x, w1, b1, w2, idx, counts, k_max, chunk, batch, n, d, f, act_cm,
-                              out_cache, delta_ws, k_pad, s);
+                              out_cache, delta_ws, k_pad, s, x_mid, x_out);
     return launch_smlp<1>(x, w1, b1, w2, idx, counts, k_max, chunk, batch, n, d, f, act_cm,
-                          out_cache, delta_ws, k_pad, s);
+                          out_cache, delta_ws, k_pad, s, x_mid, x_out);
 }
 
 }  // namespace dev

@@ -42,84 +42,44 @@ cudaError_t prod_absdiff(const float* a, const float* b, int64_t numel, float* o
     return cudaGetLastError();
 }
 
-// chunk means of bf16 x -> fp32 [B*C, D]
-__global__ void k_chunk_mean_bf16(const __nv_bfloat16* x, int64_t n, int64_t d, int64_t chunk,
-                                  int64_t bc_total, float* out) {
-    const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t bc = blockIdx.y;
-    if (col >= d || bc >= bc_total) return;
-    const int64_t nc = n / chunk;
-    const int64_t b = bc / nc, c = bc % nc;
-    const __nv_bfloat16* src = x + (b * n + c * chunk) * d + col;
-    float s = 0.f;
-    for (int64_t r = 0; r < chunk; ++r) s += __bfloat162float(src[r * d]);
-    out[bc * d + col] = s * (1.0f / (float)chunk);
-}
-
-constexpr int GT = 64, GK = 32;
-
-// T[bc, f] = means[bc, :] . W1[f, :]   grid (F/64, ceil(BC/64))
+// Dense-step MLP epilogue, fused (mlp.cpp:57-62 + cache refresh mlp.cpp:196-205):
+// pre (bf16 [B*N, F], from the dense GEMM1) -> act = gelu(pre + b1) written row-major
+// (GEMM2 operand) AND transposed into the chunk-major activation cache [B,C,F,chunk],
+// through a 64x64 shared-memory tile so both writes are coalesced.
 __global__ void __launch_bounds__(256)
-k_means_w1(const float* __restrict__ means, const __nv_bfloat16* __restrict__ w1, int64_t bc,
-           int64_t d, int64_t f, float* __restrict__ out) {
-    __shared__ float As[GK][GT + 1];
-    __shared__ float Bs[GK][GT + 1];
-    const int64_t n0 = (int64_t)blockIdx.x * GT, m0 = (int64_t)blockIdx.y * GT;
-    const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-    float acc[4][4] = {};
-    for (int64_t k0 = 0; k0 < d; k0 += GK) {
-        for (int i = tid; i < GT * GK; i += 256) {
-            const int r = i / GK, kk = i % GK;
-            const int64_t gm = m0 + r, gn = n0 + r, gk = k0 + kk;
-            As[kk][r] = (gm < bc && gk < d) ? means[gm * d + gk] : 0.f;
-            Bs[kk][r] = (gn < f && gk < d) ? __bfloat162float(w1[gn * d + gk]) : 0.f;
-        }
-        __syncthreads();
-#pragma unroll 8
-        for (int kk = 0; kk < GK; ++kk) {
-            float av[4], bv[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { av[i] = As[kk][ty * 4 + i]; bv[i] = Bs[kk][tx * 4 + i]; }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj) acc[i][jj] += av[i] * bv[jj];
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int64_t r = m0 + ty * 4 + i;
-        if (r >= bc) continue;
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-            const int64_t col = n0 + tx * 4 + jj;
-            if (col < f) out[r * f + col] = acc[i][jj];
-        }
-    }
-}
-
-cudaError_t prod_tile_means(const void* x, const void* w1, int64_t batch, int64_t n, int64_t d,
-                            int64_t f, int64_t chunk, float* means_ws, float* out,
-                            cudaStream_t s) {
-    const int64_t bc = batch * (n / chunk);
-    dim3 g((unsigned)((d + 127) / 128), (unsigned)bc);
-    k_chunk_mean_bf16<<<g, 128, 0, s>>>((const __nv_bfloat16*)x, n, d, chunk, bc, means_ws);
-    dim3 g2((unsigned)((f + GT - 1) / GT), (unsigned)((bc + GT - 1) / GT));
-    k_means_w1<<<g2, 256, 0, s>>>(means_ws, (const __nv_bfloat16*)w1, bc, d, f, out);
-    return cudaGetLastError();
-}
-
-// act [B*N, F] bf16 (row-major, from the dense GEMM1) -> chunk-major cache
-__global__ void k_act_to_cm(const __nv_bfloat16* act, int64_t n, int64_t f, int64_t chunk,
-                            int64_t total_rows, __nv_bfloat16* cm) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= total_rows * f) return;
-    const int64_t row = i / f, col = i % f;      // row = b*n + tok
-    const int64_t b = row / n, tok = row % n;
-    const int64_t c = tok / chunk, r = tok % chunk;
+k_bias_gelu_cm(const __nv_bfloat16* __restrict__ pre, const float* __restrict__ b1, int64_t n,
+               int64_t f, int64_t chunk, __nv_bfloat16* __restrict__ act,
+               __nv_bfloat16* __restrict__ cm) {
+    __shared__ __nv_bfloat16 tile[64][66];
+    const int64_t z = blockIdx.z;  // b * C + c
     const int64_t nc = n / chunk;
-    cm[(((b * nc + c) * f) + col) * chunk + r] = act[i];
+    const int64_t b = z / nc, c = z % nc;
+    const int64_t r0 = (int64_t)blockIdx.y * 64, f0 = (int64_t)blockIdx.x * 64;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    // row-major pass: each thread 2 columns, rows ty, ty+8, ...
+    for (int rr = ty; rr < 64; rr += 8) {
+        const int64_t r = r0 + rr;
+        if (r >= chunk) break;
+        const int64_t row = b * n + c * chunk + r;
+        const int64_t col = f0 + 2 * tx;
+        if (col + 1 < f + 1) {
+            const __nv_bfloat162 p2 = *reinterpret_cast<const __nv_bfloat162*>(pre + row * f + col);
+            const float2 pf = __bfloat1622float2(p2);
+            const __nv_bfloat162 a2 =
+                __floats2bfloat162_rn(fast_gelu(pf.x + b1[col]), fast_gelu(pf.y + b1[col + 1]));
+            *reinterpret_cast<__nv_bfloat162*>(act + row * f + col) = a2;
+            tile[rr][2 * tx] = a2.x;
+            tile[rr][2 * tx + 1] = a2.y;
+        }
+    }
+    __syncthreads();
+    // chunk-major pass: cm[z][f0 + j][r0 + i], contiguous along i
+    for (int jj = ty; jj < 64; jj += 8) {
+        const int64_t col = f0 + jj;
+        __nv_bfloat16* dst = cm + (z * f + col) * chunk + r0;
+        for (int i = tx; i < 64; i += 32)
+            if (r0 + i < chunk) dst[i] = tile[i][jj];
+    }
 }
 __global__ void k_cm_to_ref(const __nv_bfloat16* cm, int64_t n, int64_t f, int64_t chunk,
                             int64_t total_rows, float* out) {
@@ -139,35 +99,29 @@ cudaError_t prod_act_cm_to_ref(const void* act_cm, int64_t batch, int64_t n, int
     return cudaGetLastError();
 }
 
-// gelu + bias epilogue for the cuBLAS dense GEMM1: pre (fp32 [BN, F]) -> act bf16
-__global__ void k_bias_gelu(const float* pre, const float* b1, int64_t rows, int64_t f,
-                            __nv_bfloat16* act) {
+// out (fp32 M_cache) += b2 per row; optionally x_out = bf16(x_mid + out) in the same pass
+__global__ void k_bias_add_rows(float* out, const float* b2, int64_t rows, int64_t d,
+                                const __nv_bfloat16* x_mid, __nv_bfloat16* x_out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= rows * f) return;
-    act[i] = __float2bfloat16_rn(fast_gelu(pre[i] + b1[i % f]));
-}
-__global__ void k_bias_add_rows(float* out, const float* b2, int64_t rows, int64_t d) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < rows * d) out[i] += b2[i % d];
+    if (i >= rows * d) return;
+    const float v = out[i] + b2[i % d];
+    out[i] = v;
+    if (x_out) x_out[i] = __float2bfloat16_rn(__bfloat162float(x_mid[i]) + v);
 }
 
-cudaError_t prod_bias_gelu(const float* pre, const float* b1, int64_t rows, int64_t f, void* act,
-                           cudaStream_t s) {
-    const int64_t t = rows * f;
-    k_bias_gelu<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(pre, b1, rows, f, (__nv_bfloat16*)act);
+cudaError_t prod_bias_gelu_cm(const void* pre, const float* b1, int64_t batch, int64_t n,
+                              int64_t f, int64_t chunk, void* act, void* cm, cudaStream_t s) {
+    if (f % 64) return cudaErrorNotSupported;
+    dim3 g((unsigned)(f / 64), (unsigned)((chunk + 63) / 64), (unsigned)(batch * (n / chunk)));
+    k_bias_gelu_cm<<<g, 256, 0, s>>>((const __nv_bfloat16*)pre, b1, n, f, chunk,
+                                     (__nv_bfloat16*)act, (__nv_bfloat16*)cm);
     return cudaGetLastError();
 }
 cudaError_t prod_bias_add_rows(float* out, const float* b2, int64_t rows, int64_t d,
-                               cudaStream_t s) {
+                               const void* x_mid, void* x_out, cudaStream_t s) {
     const int64_t t = rows * d;
-    k_bias_add_rows<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(out, b2, rows, d);
-    return cudaGetLastError();
-}
-cudaError_t prod_act_to_cm(const void* act, int64_t batch, int64_t n, int64_t f, int64_t chunk,
-                           void* cm, cudaStream_t s) {
-    const int64_t tot = batch * n * f;
-    k_act_to_cm<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>((const __nv_bfloat16*)act, n, f,
-                                                            chunk, batch * n, (__nv_bfloat16*)cm);
+    k_bias_add_rows<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(
+        out, b2, rows, d, (const __nv_bfloat16*)x_mid, (__nv_bfloat16*)x_out);
     return cudaGetLastError();
 }
 

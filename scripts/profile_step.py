@@ -3,7 +3,7 @@
     ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/launches.csv python scripts/profile_step.py
 Runs: dense (init), sparse x2 (warm), then the profiled pair: one dense + one sparse step.
-Optional --only attn : just the sparse attention kernel on the FLUX shape (for --set full).
+--only sparse|dense: profile a single step of that kind (use ncu --profile-from-start off).
 """
 import argparse
 import os
@@ -20,7 +20,7 @@ from paper_2506_03275_b200 import ops  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="step", choices=["step", "attn", "mlp"])
+    ap.add_argument("--only", default="step", choices=["step", "sparse", "dense"])
     args = ap.parse_args()
     cfg = dict(bench.FLUX)
     n = cfg["grid"][1] * cfg["grid"][2]
@@ -34,10 +34,13 @@ def main():
     for dense in (True, False, False):
         blk.step(x, dense, out=y)
     torch.cuda.synchronize()
-    for dense in (True, False):
+    kinds = {"step": (True, False), "sparse": (False,), "dense": (True,)}[args.only]
+    torch.cuda.profiler.start()  # ncu --profile-from-start off captures only this window
+    for dense in kinds:
         blk.step(x, dense, out=y)
     torch.cuda.synchronize()
-    print("profiled 1 dense + 1 sparse step", flush=True)
+    torch.cuda.profiler.stop()
+    print("profiled steps:", kinds, flush=True)
 
 
 if __name__ == "__main__":
