@@ -1,25 +1,26 @@
 // attn_tc.cu — column-sparse attention on tcgen05 (CSD_MODE_PROD).
 //
 // Replaces sparse_delta_attention (attention.cpp:147-194), dense_attention
-// (:59-74) and the dense-step column sums (:76-145) with ONE kernel family:
+// (:59-74) and the dense-step column sums (:76-145) with ONE kernel family.
 //
-//   work item = (b, h, query chunk c): Q_c is 128- or 256-row (NT = 1 or 2
-//   M-tiles of 128; c = 192 uses 2 tiles with 64 idle rows), keys are the
-//   chunk's index list (sparse) or all N keys (dense baseline / dense step).
-//   For each 128-key block j:
-//     producer warp : TMA gather4 of the selected K and V rows (4 rows per
-//                     instruction, two 64-column 128B-swizzled strips at
-//                     E = 128) — or plain TMA tiles in dense mode;
-//     MMA thread    : S_t = Q_t K_j^T  (tcgen05.mma M128 N128 K16, TMEM acc);
-//     softmax warps : one thread per query row (TMEM lane), online softmax
-//                     over the SUBSET with lazy rescaling (only when the row
-//                     max grows by > 2^8), P_t -> smem bf16 (swizzled);
-//                     optional column sums with stale stats (dense step);
-//     MMA thread    : O_t += P_t V_j  (V as MN-major B operand).
-//   Epilogue: out = base + scale * O / l   (the O = O_cache + delta update,
-//   north_star item 5) and the softmax stats (row max / exp sum).
+// Work item = (b, h, query chunk c); Q_c is NT = 1 or 2 M-tiles of 128 rows (c = 192
+// uses 2 tiles, 64 idle rows); keys are the chunk's index list (sparse) or all N keys
+// (dense baseline / dense step).  Per 128-key block j:
+//   producer warp : TMA gather4 of the selected K and V rows (4 rows per instruction,
+//                   two 64-column 128B-swizzled strips at E = 128) into a 2-deep ring —
+//                   or plain TMA tiles in dense mode;
+//   MMA thread    : S_t = Q_t K_j^T  (tcgen05.mma M128 N128 K16, fp32 in TMEM), then
+//                   O_t += P_t V_j with P_t read straight from TMEM (TS form; V is the
+//                   MN-major smem operand).  The two tiles ping-pong: S_0(j+1) is issued
+//                   right after PV_0(j), so tile 0's MMAs overlap tile 1's softmax.
+//   softmax warps : one thread per query row (TMEM lane); online softmax over the
+//                   SUBSET with lazy rescaling (only when the row max grows by > 2^8),
+//                   P_t written back as bf16 over the first 64 columns of S_t;
+//                   dense step: chunk column sums with stale stats (warp transpose-reduce).
+//   Epilogue: out = base + scale * O / l (the cache update O = O_cache + delta,
+//   north_star item 5; base prefetched while the last P·V runs) and row max / exp-sum.
 //
-// TMEM: S tiles at columns [0, 128*NT), O tiles at [128*NT, 128*NT + E*NT).
+// TMEM: S_t (and P_t aliased) at columns [128 t, 128 t + 128); O_t at [128 NT + E t, +E).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -44,11 +45,11 @@ template <int E, int NT>
 struct AttnLayout {
     static constexpr int kHalves = E / 64;
     static constexpr uint32_t kStrip = 128 * 128;  // 128 rows x 128 B
+    static constexpr uint32_t kKV = kHalves * kStrip;  // one K or V block
     static constexpr uint32_t kQ = 0;
-    static constexpr uint32_t kK = kQ + NT * kHalves * kStrip;
-    static constexpr uint32_t kV = kK + kHalves * kStrip;
-    static constexpr uint32_t kP = kV + kHalves * kStrip;
-    static constexpr uint32_t kCs = kP + NT * 2 * kStrip;
+    static constexpr uint32_t kK = kQ + NT * kHalves * kStrip;  // [2] ring
+    static constexpr uint32_t kV = kK + 2 * kKV;                // [2] ring
+    static constexpr uint32_t kCs = kV + 2 * kKV;
     static constexpr uint32_t kBar = kCs + 2 * 4 * NT * 128 * 4;
     static constexpr uint32_t kBytes = kBar + 256;
     static constexpr uint32_t kSmemAlloc = kBytes + 1024;  // manual 1 KB alignment
@@ -116,23 +117,27 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
 
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
     uint64_t* bar_q = bars + 0;
-    uint64_t* bar_kf = bars + 1;
-    uint64_t* bar_ke = bars + 2;
-    uint64_t* bar_vf = bars + 3;
-    uint64_t* bar_ve = bars + 4;
-    uint64_t* bar_s = bars + 5;
-    uint64_t* bar_p = bars + 6;
-    uint64_t* bar_o = bars + 7;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    uint64_t* bar_kf = bars + 1;   // [2]
+    uint64_t* bar_ke = bars + 3;   // [2]
+    uint64_t* bar_vf = bars + 5;   // [2]
+    uint64_t* bar_ve = bars + 7;   // [2]
+    uint64_t* bar_s = bars + 9;    // [NT]
+    uint64_t* bar_p = bars + 11;   // [NT]
+    uint64_t* bar_o = bars + 13;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
     if (threadIdx.x == 0) {
         mbar_init(bar_q, 1);
-        mbar_init(bar_kf, 1);
-        mbar_init(bar_ke, 1);
-        mbar_init(bar_vf, 1);
-        mbar_init(bar_ve, 1);
-        mbar_init(bar_s, 1);
-        mbar_init(bar_p, 128 * NT);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(bar_kf + i, 1);
+            mbar_init(bar_ke + i, 1);
+            mbar_init(bar_vf + i, 1);
+            mbar_init(bar_ve + i, 1);
+        }
+        for (int t = 0; t < NT; ++t) {
+            mbar_init(bar_s + t, 1);
+            mbar_init(bar_p + t, 128);
+        }
         mbar_init(bar_o, 1);
         fence_barrier_init();
     }
@@ -156,41 +161,44 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         }
         const int32_t* ids = dense ? nullptr : p.idx + (int64_t)item * p.k_max;
         for (int j = 0; j < nblk; ++j) {
+            const int s = j & 1;
             int32_t rows[4];
             if (!dense) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     int r = j * 128 + lane * 4 + i;
                     r = r < cnt ? r : cnt - 1;  // pad with a valid row (masked in softmax)
-                    rows[i] = row_base + ids[r];
+                    rows[i] = row_base + __ldg(ids + r);
                 }
             }
-            // K_j
-            if (j > 0) mbar_wait(bar_ke, (j - 1) & 1);
-            if (lane == 0) mbar_arrive_expect_tx(bar_kf, L::kHalves * L::kStrip);
+            // K_j -> ring slot s
+            if (j >= 2) mbar_wait(bar_ke + s, ((j >> 1) - 1) & 1);
+            if (lane == 0) mbar_arrive_expect_tx(bar_kf + s, L::kKV);
             __syncwarp();
+            uint8_t* kdst = smem + L::kK + s * L::kKV;
             if (dense) {
                 if (lane == 0)
                     for (int hf = 0; hf < L::kHalves; ++hf)
-                        tma_load_2d(&tm_k, bar_kf, smem + L::kK + hf * L::kStrip, col0 + hf * 64,
+                        tma_load_2d(&tm_k, bar_kf + s, kdst + hf * L::kStrip, col0 + hf * 64,
                                     row_base + j * 128);
             } else {
                 for (int hf = 0; hf < L::kHalves; ++hf)
-                    tma_gather4(&tm_kg, bar_kf, smem + L::kK + hf * L::kStrip + lane * 512,
+                    tma_gather4(&tm_kg, bar_kf + s, kdst + hf * L::kStrip + lane * 512,
                                 col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
             }
-            // V_j
-            if (j > 0) mbar_wait(bar_ve, (j - 1) & 1);
-            if (lane == 0) mbar_arrive_expect_tx(bar_vf, L::kHalves * L::kStrip);
+            // V_j -> ring slot s
+            if (j >= 2) mbar_wait(bar_ve + s, ((j >> 1) - 1) & 1);
+            if (lane == 0) mbar_arrive_expect_tx(bar_vf + s, L::kKV);
             __syncwarp();
+            uint8_t* vdst = smem + L::kV + s * L::kKV;
             if (dense) {
                 if (lane == 0)
                     for (int hf = 0; hf < L::kHalves; ++hf)
-                        tma_load_2d(&tm_v, bar_vf, smem + L::kV + hf * L::kStrip, col0 + hf * 64,
+                        tma_load_2d(&tm_v, bar_vf + s, vdst + hf * L::kStrip, col0 + hf * 64,
                                     row_base + j * 128);
             } else {
                 for (int hf = 0; hf < L::kHalves; ++hf)
-                    tma_gather4(&tm_vg, bar_vf, smem + L::kV + hf * L::kStrip + lane * 512,
+                    tma_gather4(&tm_vg, bar_vf + s, vdst + hf * L::kStrip + lane * 512,
                                 col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
             }
         }
@@ -200,37 +208,47 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
             constexpr uint32_t idO = idesc_bf16(128, E, false, true);
             const uint32_t sQ = smem_u32(smem + L::kQ), sK = smem_u32(smem + L::kK);
-            const uint32_t sV = smem_u32(smem + L::kV), sP = smem_u32(smem + L::kP);
+            const uint32_t sV = smem_u32(smem + L::kV);
+            auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
+                const uint32_t kb = sK + (j & 1) * L::kKV;
+#pragma unroll
+                for (int kk = 0; kk < E / 16; ++kk)
+                    mma_bf16(tmem + t * 128,
+                             desc_kmajor_sw128(sQ + (t * L::kHalves + kk / 4) * L::kStrip + (kk % 4) * 32),
+                             desc_kmajor_sw128(kb + (kk / 4) * L::kStrip + (kk % 4) * 32), idS,
+                             kk > 0 ? 1u : 0u);
+                mma_commit(bar_s + t);
+            };
+            auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j, P_t from TMEM
+                const uint32_t vb = sV + (j & 1) * L::kKV;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_bf16_ts(tmem + NT * 128 + t * E, tmem + t * 128 + kk * 8,
+                                desc_mnmajor_sw128(vb + kk * 2048, L::kStrip), idO,
+                                (j > 0 || kk > 0) ? 1u : 0u);
+            };
             mbar_wait(bar_q, 0);
+            mbar_wait(bar_kf, 0);
+            tc_fence_after();
+            for (int t = 0; t < NT; ++t) issue_s(t, 0);
+            mma_commit(bar_ke + 0);
             for (int j = 0; j < nblk; ++j) {
-                mbar_wait(bar_kf, j & 1);
-                tc_fence_after();
+                const bool more = j + 1 < nblk;
                 for (int t = 0; t < NT; ++t) {
-#pragma unroll
-                    for (int kk = 0; kk < E / 16; ++kk) {
-                        const uint64_t a = desc_kmajor_sw128(
-                            sQ + (t * L::kHalves + kk / 4) * L::kStrip + (kk % 4) * 32);
-                        const uint64_t bd =
-                            desc_kmajor_sw128(sK + (kk / 4) * L::kStrip + (kk % 4) * 32);
-                        mma_bf16(tmem + t * 128, a, bd, idS, kk > 0 ? 1u : 0u);
+                    mbar_wait(bar_p + t, j & 1);  // P_t(j) in TMEM, O_t rescaled
+                    if (t == 0) mbar_wait(bar_vf + (j & 1), (j >> 1) & 1);
+                    tc_fence_after();
+                    issue_pv(t, j);
+                    if (t == NT - 1) mma_commit(bar_ve + (j & 1));
+                    if (more) {
+                        if (t == 0) {
+                            mbar_wait(bar_kf + ((j + 1) & 1), ((j + 1) >> 1) & 1);
+                            tc_fence_after();
+                        }
+                        issue_s(t, j + 1);  // in-order after PV_t(j): P_t consumed first
+                        if (t == NT - 1) mma_commit(bar_ke + ((j + 1) & 1));
                     }
                 }
-                mma_commit(bar_ke);
-                mma_commit(bar_s);
-                mbar_wait(bar_p, j & 1);
-                mbar_wait(bar_vf, j & 1);
-                tc_fence_after();
-                for (int t = 0; t < NT; ++t) {
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        const uint64_t a =
-                            desc_kmajor_sw128(sP + (t * 2 + kk / 4) * L::kStrip + (kk % 4) * 32);
-                        const uint64_t bd = desc_mnmajor_sw128(sV + kk * 2048, L::kStrip);
-                        mma_bf16(tmem + NT * 128 + t * E, a, bd, idO,
-                                 (j > 0 || kk > 0) ? 1u : 0u);
-                    }
-                }
-                mma_commit(bar_ve);
             }
             mma_commit(bar_o);
         }
@@ -245,7 +263,6 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const uint32_t tS = tmem + lane_off + t * 128;
         const uint32_t tO = tmem + lane_off + NT * 128 + t * E;
-        uint8_t* sPt = smem + L::kP + t * 2 * L::kStrip;
         float* cs_part = reinterpret_cast<float*>(smem + L::kCs);
         const int64_t tok = (int64_t)c * p.chunk + crow;
         const bool do_cs = p.colsum != nullptr;
@@ -255,18 +272,10 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             mpl = p.prev_m[si] * kLog2e;
             inv_lp = 1.0f / p.prev_l[si];
         }
-        if (!warp_ok) {  // idle rows: P rows stay zero for the whole item
-#pragma unroll
-            for (int c16 = 0; c16 < 8; ++c16) {
-                *reinterpret_cast<uint4*>(sPt + sw128_offset(row_t, c16)) = make_uint4(0, 0, 0, 0);
-                *reinterpret_cast<uint4*>(sPt + L::kStrip + sw128_offset(row_t, c16)) =
-                    make_uint4(0, 0, 0, 0);
-            }
-        }
         float m_run = -INFINITY, m_true = -INFINITY, l_run = 0.f;
         const float sl2 = p.qk_scale_log2;
         for (int j = 0; j < nblk; ++j) {
-            mbar_wait(bar_s, j & 1);
+            mbar_wait(bar_s + t, j & 1);
             tc_fence_after();
             const int ncols = min(128, cnt - j * 128);
             if (warp_ok) {
@@ -284,12 +293,12 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 }
                 m_true = fmaxf(m_true, mx);
                 const bool need = mx > m_run + kRescaleThreshold;
-                const float alpha = need ? exp2f(m_run - mx) : 1.0f;
+                const float alpha = need ? ex2_approx(m_run - mx) : 1.0f;
                 if (need) {
                     m_run = mx;
                     l_run *= alpha;
                 }
-                if (j > 0 && __any_sync(0xffffffffu, need)) {
+                if (j > 0 && __any_sync(0xffffffffu, need)) {  // PV_t(j-1) done (bar_s order)
 #pragma unroll
                     for (int oc = 0; oc < E / 32; ++oc) {
                         tmem_ld32(tO + oc * 32, r);
@@ -299,9 +308,8 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                             r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
                         tmem_st32(tO + oc * 32, r);
                     }
-                    tmem_st_wait();
                 }
-                const float w = do_cs ? exp2f(m_run - mpl) * inv_lp : 0.f;
+                const float w = do_cs ? ex2_approx(m_run - mpl) * inv_lp : 0.f;
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
                     tmem_ld32(tS + cc * 32, r);
@@ -311,20 +319,15 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const bool ok = row_ok && (cc * 32 + i < ncols);
-                        pv[i] = ok ? exp2f(__uint_as_float(r[i]) * sl2 - m_run) : 0.f;
+                        pv[i] = ok ? ex2_approx(__uint_as_float(r[i]) * sl2 - m_run) : 0.f;
                         part += pv[i];
                     }
                     l_run += part;
-                    uint8_t* half = sPt + (cc >> 1) * L::kStrip;
+                    // P_t (bf16 pairs) over S_t columns [16 cc, 16 cc + 16) — already read
+                    uint32_t pk[16];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        uint4 v;
-                        v.x = pack_bf16x2(pv[q * 8 + 0], pv[q * 8 + 1]);
-                        v.y = pack_bf16x2(pv[q * 8 + 2], pv[q * 8 + 3]);
-                        v.z = pack_bf16x2(pv[q * 8 + 4], pv[q * 8 + 5]);
-                        v.w = pack_bf16x2(pv[q * 8 + 6], pv[q * 8 + 7]);
-                        *reinterpret_cast<uint4*>(half + sw128_offset(row_t, (cc & 1) * 4 + q)) = v;
-                    }
+                    for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(pv[2 * q], pv[2 * q + 1]);
+                    tmem_st16(tS + cc * 16, pk);
                     if (do_cs) {
                         // transpose-reduce the warp's 32x32 block: lane ends with column `lane`
 #pragma unroll
@@ -342,10 +345,17 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                         cs_part[((j & 1) * 4 * NT + sw) * 128 + cc * 32 + lane] = pv[0];
                     }
                 }
+            } else {
+                // rows past the chunk: zero P so the padded MMA rows stay finite
+                uint32_t pk[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) pk[q] = 0u;
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) tmem_st16(tS + cc * 16, pk);
             }
-            fence_proxy_async_smem();
+            tmem_st_wait();
             tc_fence_before();
-            mbar_arrive(bar_p);
+            mbar_arrive(bar_p + t);
             if (do_cs) {
                 named_bar_sync(1, 128 * NT);
                 const int st = sw * 32 + lane;
@@ -358,11 +368,18 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             }
         }
         // ------------------------------------------------------------ epilogue
+        const int64_t off = tok_elem_off(p.layout, b, h, tok, p.heads, p.n, E);
+        uint4 bpre[E / 8];  // prefetch base while the last P.V runs
+        const bool has_base = p.base != nullptr;
+        if (warp_ok && row_ok && has_base) {
+            const uint4* bp = reinterpret_cast<const uint4*>(p.base + off);
+#pragma unroll
+            for (int q = 0; q < E / 8; ++q) bpre[q] = __ldg(bp + q);
+        }
         mbar_wait(bar_o, 0);
         tc_fence_after();
         if (warp_ok) {
             const float inv_l = 1.0f / l_run;
-            const int64_t off = tok_elem_off(p.layout, b, h, tok, p.heads, p.n, E);
 #pragma unroll
             for (int oc = 0; oc < E / 32; ++oc) {
                 uint32_t r[32];
@@ -372,12 +389,11 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                     float o[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r[i]) * inv_l;
-                    if (p.base != nullptr) {
-                        const uint4* bp = reinterpret_cast<const uint4*>(p.base + off + oc * 32);
+                    if (has_base) {
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const uint4 bv = bp[q];
-                            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bv);
+                            const __nv_bfloat162* b2 =
+                                reinterpret_cast<const __nv_bfloat162*>(&bpre[oc * 4 + q]);
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
                                 const float2 f = __bfloat1622float2(b2[u]);
