@@ -147,9 +147,14 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
-        // ------------------------------------------------------------ producer
-        if (lane == 0) {
+    if (warp == 0 || warp == 2 || warp == 3) {
+        // ------------------------------------------------------------ producers
+        // TMA instructions issued by one warp are serialised lane by lane (~85 cycles each,
+        // scripts/gather_bench.cu), so the 128 gather4s per key block are spread over the
+        // three non-MMA warps: producer pw issues the row groups g with g % 3 == pw.
+        const int pw = warp == 0 ? 0 : warp - 1;
+        const bool mine = (lane % 3) == pw;
+        if (warp == 0 && lane == 0) {
             tma_prefetch_desc(&tm_q);
             tma_prefetch_desc(dense ? &tm_k : &tm_kg);
             tma_prefetch_desc(dense ? &tm_v : &tm_vg);
@@ -173,30 +178,28 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             }
             // K_j -> ring slot s
             if (j >= 2) mbar_wait(bar_ke + s, ((j >> 1) - 1) & 1);
-            if (lane == 0) mbar_arrive_expect_tx(bar_kf + s, L::kKV);
-            __syncwarp();
+            if (warp == 0 && lane == 0) mbar_arrive_expect_tx(bar_kf + s, L::kKV);
             uint8_t* kdst = smem + L::kK + s * L::kKV;
             if (dense) {
-                if (lane == 0)
+                if (warp == 0 && lane == 0)
                     for (int hf = 0; hf < L::kHalves; ++hf)
                         tma_load_2d(&tm_k, bar_kf + s, kdst + hf * L::kStrip, col0 + hf * 64,
                                     row_base + j * 128);
-            } else {
+            } else if (mine) {
                 for (int hf = 0; hf < L::kHalves; ++hf)
                     tma_gather4(&tm_kg, bar_kf + s, kdst + hf * L::kStrip + lane * 512,
                                 col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
             }
             // V_j -> ring slot s
             if (j >= 2) mbar_wait(bar_ve + s, ((j >> 1) - 1) & 1);
-            if (lane == 0) mbar_arrive_expect_tx(bar_vf + s, L::kKV);
-            __syncwarp();
+            if (warp == 0 && lane == 0) mbar_arrive_expect_tx(bar_vf + s, L::kKV);
             uint8_t* vdst = smem + L::kV + s * L::kKV;
             if (dense) {
-                if (lane == 0)
+                if (warp == 0 && lane == 0)
                     for (int hf = 0; hf < L::kHalves; ++hf)
                         tma_load_2d(&tm_v, bar_vf + s, vdst + hf * L::kStrip, col0 + hf * 64,
                                     row_base + j * 128);
-            } else {
+            } else if (mine) {
                 for (int hf = 0; hf < L::kHalves; ++hf)
                     tma_gather4(&tm_vg, bar_vf + s, vdst + hf * L::kStrip + lane * 512,
                                 col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);

@@ -124,29 +124,33 @@ k_smlp_up(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUte
     uint32_t tmem;
     mlp_setup<NT>(smem, full, empty, done, tmem);
 
-    if (warp == 0) {
+    if (warp == 0 || warp == 2 || warp == 3) {
+        // producers: warp 0 issues the x tiles; the 32 W1-row gather4s per stage are spread
+        // over warps 0/2/3 (one warp's TMA issue is serialised, scripts/gather_bench.cu)
+        const int pw = warp == 0 ? 0 : warp - 1;
+        const bool mine = (lane % 3) == pw;
         int32_t rows[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             int nn = tn * 128 + lane * 4 + i;
             rows[i] = ids[nn < cnt ? nn : cnt - 1];
         }
-        if (lane == 0) {
+        if (warp == 0 && lane == 0) {
             tma_prefetch_desc(&tm_x);
             tma_prefetch_desc(&tm_w1g);
         }
         for (int kb = 0; kb < kblocks; ++kb) {
             const int s = kb % kMlpStages;
             if (kb >= kMlpStages) mbar_wait(empty + s, ((kb / kMlpStages) - 1) & 1);
-            if (lane == 0) {
+            if (warp == 0 && lane == 0) {
                 mbar_arrive_expect_tx(full + s, (NT + 1) * kTile);
                 for (int t = 0; t < NT; ++t)
                     tma_load_2d(&tm_x, full + s, smem + L::kA + (s * NT + t) * kTile, kb * 64,
                                 x_row0 + t * 128);
             }
-            __syncwarp();
-            tma_gather4(&tm_w1g, full + s, smem + L::kB + s * kTile + lane * 512, kb * 64, rows[0],
-                        rows[1], rows[2], rows[3]);
+            if (mine)
+                tma_gather4(&tm_w1g, full + s, smem + L::kB + s * kTile + lane * 512, kb * 64,
+                            rows[0], rows[1], rows[2], rows[3]);
         }
     } else if (warp == 1) {
         if (lane == 0) {
@@ -265,8 +269,10 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta,
     uint32_t tmem;
     mlp_setup<NT>(smem, full, empty, done, tmem);
 
-    if (warp == 0) {
-        if (lane == 0) {
+    if (warp == 0 || warp == 2 || warp == 3) {
+        const int pw = warp == 0 ? 0 : warp - 1;
+        const bool mine = (lane % 3) == pw;
+        if (warp == 0 && lane == 0) {
             tma_prefetch_desc(&tm_delta);
             tma_prefetch_desc(&tm_w2g);
         }
@@ -280,16 +286,16 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta,
                 rows[i] = ids[nn < cnt ? nn : cnt - 1];
             }
             if (kb >= kMlpStages) mbar_wait(empty + s, ((kb / kMlpStages) - 1) & 1);
-            if (lane == 0) {
+            if (warp == 0 && lane == 0) {
                 mbar_arrive_expect_tx(full + s, (NT + 1) * kTile);
                 for (int t = 0; t < NT; ++t)
                     tma_load_2d(&tm_delta, full + s, smem + L::kA + (s * NT + t) * kTile, kb * 64,
                                 z * p.chunk + t * 128);
             }
-            __syncwarp();
             // B tile: 64 neuron rows x 128 D columns as two 64-column (128 B) strips of 8 KB
-            tma_gather4(&tm_w2g, full + s, smem + L::kB + s * kTile + strip * 8192 + g4 * 512,
-                        td * 128 + strip * 64, rows[0], rows[1], rows[2], rows[3]);
+            if (mine)
+                tma_gather4(&tm_w2g, full + s, smem + L::kB + s * kTile + strip * 8192 + g4 * 512,
+                            td * 128 + strip * 64, rows[0], rows[1], rows[2], rows[3]);
         }
     } else if (warp == 1) {
         if (lane == 0) {

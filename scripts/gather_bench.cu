@@ -1,0 +1,168 @@
+// gather_bench.cu — micro-benchmark of the three ways to stage 128 scattered 128-byte rows
+// (one K/V or weight-row block) into 128B-swizzled shared memory on sm_100a:
+//   mode 0: TMA 2D tile (contiguous rows; reference point)
+//   mode 1: TMA tile::gather4, 32 instructions per block (one per lane)
+//   mode 2: cp.async 16 B by 128 threads (8 per thread), mbarrier-tracked
+// Each CTA (one per SM) streams `iters` blocks through a 4-stage ring; prints GB/s.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
+//        -I paper_2506_03275_b200/csrc scripts/gather_bench.cu -o scripts/gather_bench -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "tc_common.cuh"
+
+using namespace csd::tc;
+
+constexpr int kStages = 4;
+constexpr int kBlk = 128 * 128;
+
+__global__ void __launch_bounds__(128, 1)
+k_bench(const __grid_constant__ CUtensorMap tile_map, const __grid_constant__ CUtensorMap g4_map,
+        const __nv_bfloat16* base, int ld, const int* rows, int nrows, int iters, int mode,
+        unsigned long long* sink) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = raw + ((1024 - (smem_u32(raw) & 1023)) & 1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kBlk);
+    uint64_t* empty = full + kStages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(full + s, mode == 5 ? 128 : 1);
+            mbar_init(empty + s, 4);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    unsigned long long acc = 0;
+    for (int it = 0; it < iters; ++it) {
+        const int s = it % kStages;
+        const int rbase = ((blockIdx.x * 7919 + it * 131) % (nrows / 128)) * 128;
+        if (it >= kStages) mbar_wait(empty + s, ((it / kStages) - 1) & 1);
+        uint8_t* dst = smem + s * kBlk;
+        if (mode == 0) {
+            if (threadIdx.x == 0) {
+                mbar_arrive_expect_tx(full + s, kBlk);
+                tma_load_2d(&tile_map, full + s, dst, 0, rows[rbase]);
+            }
+        } else if (mode == 1) {
+            if (warp == 0) {
+                if (lane == 0) mbar_arrive_expect_tx(full + s, kBlk);
+                __syncwarp();
+                const int* r = rows + rbase + lane * 4;
+                tma_gather4(&g4_map, full + s, dst + lane * 512, 0, r[0], r[1], r[2], r[3]);
+            }
+        } else if (mode == 3) {
+            if (threadIdx.x == 0) mbar_arrive_expect_tx(full + s, kBlk);
+            __syncthreads();
+            if (lane < 8) {  // 4 warps x 8 lanes x gather4
+                const int g = warp * 8 + lane;
+                const int* r = rows + rbase + g * 4;
+                tma_gather4(&g4_map, full + s, dst + g * 512, 0, r[0], r[1], r[2], r[3]);
+            }
+        } else if (mode == 4) {
+            // unswizzled staging: one 128 B bulk copy per row (layout not MMA-ready; cost probe)
+            if (threadIdx.x == 0) mbar_arrive_expect_tx(full + s, kBlk);
+            __syncthreads();
+            const int row = threadIdx.x;
+            const __nv_bfloat16* src = base + (size_t)rows[rbase + row] * ld;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 128, [%2];"
+                ::"r"(smem_u32(dst + row * 128)), "l"(src), "r"(smem_u32(full + s)) : "memory");
+        } else {  // mode 5
+            // 128 threads x 8 x 16 B; row = tid, chunks 0..7 swizzled
+            const int row = threadIdx.x;
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(base + (size_t)rows[rbase + row] * ld);
+            for (int c = 0; c < 8; ++c) {
+                const uint32_t d = smem_u32(dst) + sw128_offset(row, c);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c * 16));
+            }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)));
+        }
+        // consumer: every warp waits, touches one word, releases
+        mbar_wait(full + s, (it / kStages) & 1);
+        acc += reinterpret_cast<const uint32_t*>(dst)[threadIdx.x];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+    }
+    if (acc == 0x123456789ull) sink[0] = acc;
+}
+
+int main(int argc, char** argv) {
+    const int rows_total = 1 << 17, cols = 64;  // 128 B rows (one 64-column strip)
+    const int ld = 3072;                         // real pitch: rows of a [F, 3072] weight
+    const size_t elems = (size_t)rows_total * ld;
+    __nv_bfloat16* d;
+    cudaMalloc(&d, elems * 2);
+    cudaMemset(d, 1, elems * 2);
+    std::vector<int> h(rows_total);
+    srand(1);
+    for (int i = 0; i < rows_total; ++i) h[i] = rand() % rows_total;
+    int* rows;
+    cudaMalloc(&rows, rows_total * 4);
+    cudaMemcpy(rows, h.data(), rows_total * 4, cudaMemcpyHostToDevice);
+    std::vector<int> seq(rows_total);
+    for (int i = 0; i < rows_total; ++i) seq[i] = i;
+    int* rows_seq;
+    cudaMalloc(&rows_seq, rows_total * 4);
+    cudaMemcpy(rows_seq, seq.data(), rows_total * 4, cudaMemcpyHostToDevice);
+    void* fnp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q);
+    auto enc = (PFN_cuTensorMapEncodeTiled_v12000)fnp;
+    CUtensorMap tm, tg;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows_total};
+    cuuint64_t str[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box_t[2] = {64, 128}, box_g[2] = {64, 1}, es[2] = {1, 1};
+    enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d, dims, str, box_t, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    enc(&tg, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d, dims, str, box_g, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    unsigned long long* sink;
+    cudaMalloc(&sink, 8);
+    const int smem = kStages * kBlk + 1024 + 256;
+    cudaFuncSetAttribute(k_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int iters = 2000;
+    // rows restricted to the first `l2rows` rows for the L2-resident variants
+    const int l2rows = 16384;  // 16384 x 6 KB pitch: 100 MB span, but only 2 MB touched
+    std::vector<int> hl(rows_total);
+    for (int i = 0; i < rows_total; ++i) hl[i] = rand() % l2rows;
+    int* rows_l2;
+    cudaMalloc(&rows_l2, rows_total * 4);
+    cudaMemcpy(rows_l2, hl.data(), rows_total * 4, cudaMemcpyHostToDevice);
+    struct Case { const char* name; int mode; const int* r; };
+    Case cases[] = {
+        {"tma tile (contiguous rows)", 0, rows_seq},
+        {"tma gather4 1 warp (random, DRAM)", 1, rows},
+        {"tma gather4 1 warp (random, L2)", 1, rows_l2},
+        {"tma gather4 4 warps (random, L2)", 3, rows_l2},
+        {"bulk 128B/row 4 warps (random, L2)", 4, rows_l2},
+        {"cp.async 16B (random, DRAM)", 5, rows},
+        {"cp.async 16B (random, L2)", 5, rows_l2},
+    };
+    for (const Case& cs : cases) {
+        const int mode = cs.mode;
+        const int* r = cs.r;
+        for (int rep = 0; rep < 2; ++rep) {
+            cudaEvent_t a, b;
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a);
+            k_bench<<<148, 128, smem>>>(tm, tg, d, ld, r, rows_total, iters, mode, sink);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            const double bytes = 148.0 * iters * kBlk;
+            if (rep) printf("%-38s %8.3f ms  %8.1f GB/s  (%.0f ns per 16 KB block per SM)\n", cs.name, ms,
+                            bytes / (ms * 1e-3) / 1e9, ms * 1e6 / iters);
+        }
+    }
+    cudaError_t e = cudaGetLastError();
+    printf("status: %s\n", cudaGetErrorString(e));
+    return 0;
+}
