@@ -146,7 +146,6 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-
     if (warp == 0 || warp == 2 || warp == 3) {
         // ------------------------------------------------------------ producers
         // TMA instructions issued by one warp are serialised lane by lane (~85 cycles each,
@@ -282,18 +281,26 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             tc_fence_after();
             const int ncols = min(128, cnt - j * 128);
             if (warp_ok) {
-                uint32_t r[32];
-                float mx = -INFINITY;
+                // S row in two 64-column halves (2 TMEM loads in flight, one wait each)
+                // fast path (uniform): every column and every row of this warp is live
+                const bool full = ncols == 128 && __all_sync(0xffffffffu, row_ok);
+                float mraw = -INFINITY;
 #pragma unroll
-                for (int cc = 0; cc < 4; ++cc) {
-                    tmem_ld32(tS + cc * 32, r);
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint32_t sr[64];
+                    tmem_ld32(tS + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+                    tmem_ld32(tS + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
                     tmem_ld_wait();
+                    if (!full) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const float x = (cc * 32 + i < ncols) ? __uint_as_float(r[i]) * sl2 : -INFINITY;
-                        mx = fmaxf(mx, x);
+                        for (int i = 0; i < 64; ++i)
+                            if (hf * 64 + i >= ncols) sr[i] = __float_as_uint(-INFINITY);
                     }
+#pragma unroll
+                    for (int i = 0; i < 64; i += 2)
+                        mraw = fmax3(mraw, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
                 }
+                const float mx = row_ok ? mraw * sl2 : -INFINITY;  // sl2 > 0: max commutes
                 m_true = fmaxf(m_true, mx);
                 const bool need = mx > m_run + kRescaleThreshold;
                 const float alpha = need ? ex2_approx(m_run - mx) : 1.0f;
@@ -302,8 +309,9 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                     l_run *= alpha;
                 }
                 if (j > 0 && __any_sync(0xffffffffu, need)) {  // PV_t(j-1) done (bar_s order)
-#pragma unroll
+#pragma unroll 1
                     for (int oc = 0; oc < E / 32; ++oc) {
+                        uint32_t r[32];
                         tmem_ld32(tO + oc * 32, r);
                         tmem_ld_wait();
 #pragma unroll
@@ -313,16 +321,18 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                     }
                 }
                 const float w = do_cs ? ex2_approx(m_run - mpl) * inv_lp : 0.f;
+                const float neg_m = row_ok ? -m_run : -INFINITY;  // dead rows -> p = 0
 #pragma unroll
                 for (int cc = 0; cc < 4; ++cc) {
-                    tmem_ld32(tS + cc * 32, r);
+                    uint32_t sr[32];
+                    tmem_ld32(tS + cc * 32, sr);
                     tmem_ld_wait();
                     float pv[32];
                     float part = 0.f;
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
-                        const bool ok = row_ok && (cc * 32 + i < ncols);
-                        pv[i] = ok ? ex2_approx(__uint_as_float(r[i]) * sl2 - m_run) : 0.f;
+                        const float x = (full || cc * 32 + i < ncols) ? __uint_as_float(sr[i]) : -INFINITY;
+                        pv[i] = ex2_approx(fmaf(x, sl2, neg_m));
                         part += pv[i];
                     }
                     l_run += part;

@@ -39,7 +39,8 @@ __global__ void k_chunk_means_split(const __nv_bfloat16* __restrict__ x, int64_t
     const int64_t b = bc / nc, c = bc % nc;
     const __nv_bfloat16* src = x + (b * n + c * chunk) * d + col;
     float s = 0.f;
-    for (int64_t r = 0; r < chunk; ++r) s += __bfloat162float(src[r * d]);
+#pragma unroll 16
+    for (int64_t r = 0; r < chunk; ++r) s += __bfloat162float(__ldg(src + r * d));
     const float mean = s * (1.0f / (float)chunk);
     const __nv_bfloat16 hi = __float2bfloat16_rn(mean);
     const __nv_bfloat16 lo = __float2bfloat16_rn(mean - __bfloat162float(hi));

@@ -28,7 +28,7 @@ using namespace csd::tc;
 bool make_map_bf16(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows,
                    uint64_t pitch_elems, uint32_t box_rows);
 
-constexpr int kMlpStages = 4;
+constexpr int kMlpStages = 2;  // 2 x 48 KB: two CTAs per SM (grid tails, TMA overlap)
 constexpr uint32_t kTile = 128 * 128;  // 128 rows x 64 bf16 (128 B) = 16 KB
 
 template <int NT>
@@ -104,7 +104,7 @@ __device__ __forceinline__ void mlp_setup(uint8_t* smem, uint64_t*& full, uint64
 
 // ------------------------------------------------------------------ up projection
 template <int NT>
-__global__ void __launch_bounds__(MlpLayout<NT>::kThreads, 1)
+__global__ void __launch_bounds__(MlpLayout<NT>::kThreads, 2)
 k_smlp_up(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w1g,
           const MlpParams p) {
     using L = MlpLayout<NT>;
@@ -236,7 +236,7 @@ k_smlp_up(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUte
 
 // ------------------------------------------------------------------ down projection
 template <int NT>
-__global__ void __launch_bounds__(MlpLayout<NT>::kThreads, 1)
+__global__ void __launch_bounds__(MlpLayout<NT>::kThreads, 2)
 k_smlp_down(const __grid_constant__ CUtensorMap tm_delta,
             const __grid_constant__ CUtensorMap tm_w2g, const MlpParams p) {
     using L = MlpLayout<NT>;

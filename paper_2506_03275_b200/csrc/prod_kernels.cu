@@ -99,14 +99,30 @@ cudaError_t prod_act_cm_to_ref(const void* act_cm, int64_t batch, int64_t n, int
     return cudaGetLastError();
 }
 
-// out (fp32 M_cache) += b2 per row; optionally x_out = bf16(x_mid + out) in the same pass
-__global__ void k_bias_add_rows(float* out, const float* b2, int64_t rows, int64_t d,
-                                const __nv_bfloat16* x_mid, __nv_bfloat16* x_out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= rows * d) return;
-    const float v = out[i] + b2[i % d];
-    out[i] = v;
-    if (x_out) x_out[i] = __float2bfloat16_rn(__bfloat162float(x_mid[i]) + v);
+// out (fp32 M_cache) += b2 per row; optionally x_out = bf16(x_mid + out) in the same pass.
+// grid (d / 4 / 256 rounded up, rows); 4 columns per thread (float4 / 8-byte bf16 accesses).
+__global__ void k_bias_add_rows(float* __restrict__ out, const float* __restrict__ b2, int64_t d,
+                                const __nv_bfloat16* __restrict__ x_mid,
+                                __nv_bfloat16* __restrict__ x_out) {
+    const int64_t row = blockIdx.y;
+    const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (col >= d) return;
+    float4* o4 = reinterpret_cast<float4*>(out + row * d + col);
+    const float4 bb = *reinterpret_cast<const float4*>(b2 + col);
+    float4 v = *o4;
+    v.x += bb.x; v.y += bb.y; v.z += bb.z; v.w += bb.w;
+    *o4 = v;
+    if (x_out) {
+        const uint2 xr = *reinterpret_cast<const uint2*>(x_mid + row * d + col);
+        const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xr);
+        const float2 a = __bfloat1622float2(xh[0]), b = __bfloat1622float2(xh[1]);
+        uint2 w;
+        __nv_bfloat162 r0 = __floats2bfloat162_rn(a.x + v.x, a.y + v.y);
+        __nv_bfloat162 r1 = __floats2bfloat162_rn(b.x + v.z, b.y + v.w);
+        w.x = *reinterpret_cast<uint32_t*>(&r0);
+        w.y = *reinterpret_cast<uint32_t*>(&r1);
+        *reinterpret_cast<uint2*>(x_out + row * d + col) = w;
+    }
 }
 
 cudaError_t prod_bias_gelu_cm(const void* pre, const float* b1, int64_t batch, int64_t n,
@@ -119,9 +135,10 @@ cudaError_t prod_bias_gelu_cm(const void* pre, const float* b1, int64_t batch, i
 }
 cudaError_t prod_bias_add_rows(float* out, const float* b2, int64_t rows, int64_t d,
                                const void* x_mid, void* x_out, cudaStream_t s) {
-    const int64_t t = rows * d;
-    k_bias_add_rows<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(
-        out, b2, rows, d, (const __nv_bfloat16*)x_mid, (__nv_bfloat16*)x_out);
+    if (d % 4) return cudaErrorNotSupported;
+    dim3 g((unsigned)((d / 4 + 255) / 256), (unsigned)rows);
+    k_bias_add_rows<<<g, 256, 0, s>>>(out, b2, d, (const __nv_bfloat16*)x_mid,
+                                      (__nv_bfloat16*)x_out);
     return cudaGetLastError();
 }
 

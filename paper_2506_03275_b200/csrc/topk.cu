@@ -80,9 +80,22 @@ k_topk_rows(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* __r
         for (int i = tid; i < 256; i += kTopkThreads) hist[i] = 0;
         __syncthreads();
         const uint32_t prefix = s_prefix;
-        for (int64_t j = tid; j < m; j += kTopkThreads) {
-            const uint32_t o = ord_key(src[j]);
-            if ((o & mask) == prefix) atomicAdd(&hist[(o >> shift) & 0xffu], 1u);
+        // warp-aggregated histogram: equal digits (common — nearby scores share exponent
+        // bytes) collapse to one shared-memory atomic per warp
+        for (int64_t j0 = 0; j0 < m; j0 += kTopkThreads) {
+            const int64_t j = j0 + tid;
+            uint32_t o = 0;
+            bool ok = false;
+            if (j < m) {
+                o = ord_key(src[j]);
+                ok = (o & mask) == prefix;
+            }
+            const uint32_t bin = (o >> shift) & 0xffu;
+            const uint32_t act = __ballot_sync(0xffffffffu, ok);
+            if (ok) {
+                const uint32_t peers = __match_any_sync(act, bin);
+                if ((tid & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+            }
         }
         __syncthreads();
         if (tid < 32) {

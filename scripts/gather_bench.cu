@@ -21,7 +21,7 @@ using namespace csd::tc;
 constexpr int kStages = 4;
 constexpr int kBlk = 128 * 128;
 
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(512, 1)
 k_bench(const __grid_constant__ CUtensorMap tile_map, const __grid_constant__ CUtensorMap g4_map,
         const __nv_bfloat16* base, int ld, const int* rows, int nrows, int iters, int mode,
         unsigned long long* sink) {
@@ -33,7 +33,7 @@ k_bench(const __grid_constant__ CUtensorMap tile_map, const __grid_constant__ CU
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(full + s, mode == 5 ? 128 : 1);
-            mbar_init(empty + s, 4);
+            mbar_init(empty + s, blockDim.x / 32);
         }
         fence_barrier_init();
     }
@@ -59,8 +59,9 @@ k_bench(const __grid_constant__ CUtensorMap tile_map, const __grid_constant__ CU
         } else if (mode == 3) {
             if (threadIdx.x == 0) mbar_arrive_expect_tx(full + s, kBlk);
             __syncthreads();
-            if (lane < 8) {  // 4 warps x 8 lanes x gather4
-                const int g = warp * 8 + lane;
+            const int nw = blockDim.x / 32, per = 32 / nw;
+            if (lane < per) {  // nw warps x (32/nw) lanes x gather4
+                const int g = warp * per + lane;
                 const int* r = rows + rbase + g * 4;
                 tma_gather4(&g4_map, full + s, dst + g * 512, 0, r[0], r[1], r[2], r[3]);
             }
@@ -69,10 +70,13 @@ k_bench(const __grid_constant__ CUtensorMap tile_map, const __grid_constant__ CU
             if (threadIdx.x == 0) mbar_arrive_expect_tx(full + s, kBlk);
             __syncthreads();
             const int row = threadIdx.x;
+            if (row >= 128) goto consume;
+            {
             const __nv_bfloat16* src = base + (size_t)rows[rbase + row] * ld;
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 128, [%2];"
                 ::"r"(smem_u32(dst + row * 128)), "l"(src), "r"(smem_u32(full + s)) : "memory");
+            }
         } else {  // mode 5
             // 128 threads x 8 x 16 B; row = tid, chunks 0..7 swizzled
             const int row = threadIdx.x;
@@ -83,6 +87,7 @@ k_bench(const __grid_constant__ CUtensorMap tile_map, const __grid_constant__ CU
             }
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)));
         }
+    consume:
         // consumer: every warp waits, touches one word, releases
         mbar_wait(full + s, (it / kStages) & 1);
         acc += reinterpret_cast<const uint32_t*>(dst)[threadIdx.x];
@@ -134,15 +139,15 @@ int main(int argc, char** argv) {
     int* rows_l2;
     cudaMalloc(&rows_l2, rows_total * 4);
     cudaMemcpy(rows_l2, hl.data(), rows_total * 4, cudaMemcpyHostToDevice);
-    struct Case { const char* name; int mode; const int* r; };
+    struct Case { const char* name; int mode; const int* r; int threads; };
     Case cases[] = {
-        {"tma tile (contiguous rows)", 0, rows_seq},
-        {"tma gather4 1 warp (random, DRAM)", 1, rows},
-        {"tma gather4 1 warp (random, L2)", 1, rows_l2},
-        {"tma gather4 4 warps (random, L2)", 3, rows_l2},
-        {"bulk 128B/row 4 warps (random, L2)", 4, rows_l2},
-        {"cp.async 16B (random, DRAM)", 5, rows},
-        {"cp.async 16B (random, L2)", 5, rows_l2},
+        {"tma tile (contiguous rows)", 0, rows_seq, 128},
+        {"tma gather4 1 warp (random, L2)", 1, rows_l2, 128},
+        {"tma gather4 4 warps x8 (random, L2)", 3, rows_l2, 128},
+        {"tma gather4 8 warps x4 (random, L2)", 3, rows_l2, 256},
+        {"tma gather4 16 warps x2 (random, L2)", 3, rows_l2, 512},
+        {"tma gather4 8 warps x4 (random, DRAM)", 3, rows, 256},
+        {"tma gather4 16 warps x2 (random, DRAM)", 3, rows, 512},
     };
     for (const Case& cs : cases) {
         const int mode = cs.mode;
@@ -152,7 +157,7 @@ int main(int argc, char** argv) {
             cudaEventCreate(&a);
             cudaEventCreate(&b);
             cudaEventRecord(a);
-            k_bench<<<148, 128, smem>>>(tm, tg, d, ld, r, rows_total, iters, mode, sink);
+            k_bench<<<148, cs.threads, smem>>>(tm, tg, d, ld, r, rows_total, iters, mode, sink);
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             float ms;
