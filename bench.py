@@ -19,7 +19,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -51,58 +50,58 @@ def k_of(n, s):
 
 # ---------------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clocks and clock-event (throttle) reasons through NVML from a
+    background thread while the timed region runs (the region is only tens of ms, so
+    `nvidia-smi -lms` would miss it)."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, device_index=0):
-        self.idx = device_index
-        self.proc = None
-        self.lines = []
+    def __init__(self, device_index=0, period_s=0.002):
+        self.idx, self.period = device_index, period_s
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[self.idx]) if vis and vis.split(",")[0].isdigit() else self.idx
+            self.h = N.nvmlDeviceGetHandleByIndex(phys)
+            self.N = N
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # no NVML: recorded as unsampled
+            self.err = str(e)
+            self.N = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.N is not None:
+            self.t.join(timeout=1)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-            except ValueError:
-                continue
-            for nm, val in zip(names, parts[5:9]):
-                if val.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"],
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "source": "NVML, 2 ms polling during the timed region"}
 
 
 # ---------------------------------------------------------------------------- ours
@@ -262,11 +261,26 @@ def run_ours(args, rank, world):
                 "achieved": round(att["alg_bytes"] / (att["ms"] * 1e-3) / 1e9, 1),
                 "peak": hbm, "peak_source": src, "unit": "GB/s",
                 "frac": round(att["alg_bytes"] / (att["ms"] * 1e-3) / 1e9 / hbm, 4),
-                "traffic": None,
+                "traffic": profiled_traffic("k_attn_tc"),
+                "traffic_unit": "bytes per launch (dram read + write, ncu --set full, "
+                                "profiles/latest_full.json)",
+                "alg_bytes": att["alg_bytes"],
                 "tensor_frac": round(att["flops"] / (att["ms"] * 1e-3) / 1e12 / tf, 4),
             },
         }
     return out
+
+
+def profiled_traffic(kernel_substr):
+    """DRAM bytes per launch of the sparse-step launch of `kernel_substr` from the committed
+    ncu --set full summary (scripts/ncu_summary.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "latest_full.json")) as f:
+            ks = [k for k in json.load(f)["kernels"] if kernel_substr in k["name"]]
+        k = min(ks, key=lambda k: k.get("duration_us", 1e30))  # the sparse (short) launch
+        return int(k["dram_traffic_MB"] * 1e6)
+    except Exception:
+        return None
 
 
 def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps):

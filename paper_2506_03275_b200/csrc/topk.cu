@@ -23,7 +23,7 @@ namespace dev {
 constexpr int kTopkThreads = 512;
 constexpr int kTopkWarps = kTopkThreads / 32;
 constexpr int64_t kTopkMaxSortK = 16384;         // 128 KB of u64 composites
-constexpr int64_t kTopkMaxSmemRow = 20 * 1024;  // fp32 elements staged in smem
+constexpr int64_t kTopkMaxSmemRow = 16 * 1024;  // fp32 elements staged in smem
 
 __device__ __forceinline__ uint32_t ord_key(float x) {
     uint32_t u = __float_as_uint(x);
@@ -76,26 +76,25 @@ k_topk_rows(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* __r
     __syncthreads();
 
     uint32_t mask = 0;
+    // per-warp private histograms: nearby scores share their top digits, so a single
+    // shared histogram serialises thousands of same-address atomics
+    __shared__ uint32_t whist[kTopkWarps][256];
+    const int warp_id = tid >> 5;
     for (int shift = 24; shift >= 0; shift -= 8) {
-        for (int i = tid; i < 256; i += kTopkThreads) hist[i] = 0;
+        for (int i = tid; i < kTopkWarps * 256; i += kTopkThreads) (&whist[0][0])[i] = 0;
         __syncthreads();
         const uint32_t prefix = s_prefix;
-        // warp-aggregated histogram: equal digits (common — nearby scores share exponent
-        // bytes) collapse to one shared-memory atomic per warp
-        for (int64_t j0 = 0; j0 < m; j0 += kTopkThreads) {
-            const int64_t j = j0 + tid;
-            uint32_t o = 0;
-            bool ok = false;
-            if (j < m) {
-                o = ord_key(src[j]);
-                ok = (o & mask) == prefix;
-            }
-            const uint32_t bin = (o >> shift) & 0xffu;
-            const uint32_t act = __ballot_sync(0xffffffffu, ok);
-            if (ok) {
-                const uint32_t peers = __match_any_sync(act, bin);
-                if ((tid & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
-            }
+        uint32_t* wh = whist[warp_id];
+        for (int64_t j = tid; j < m; j += kTopkThreads) {
+            const uint32_t o = ord_key(src[j]);
+            if ((o & mask) == prefix) atomicAdd(&wh[(o >> shift) & 0xffu], 1u);
+        }
+        __syncthreads();
+        for (int i = tid; i < 256; i += kTopkThreads) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int w = 0; w < kTopkWarps; ++w) acc += whist[w][i];
+            hist[i] = acc;
         }
         __syncthreads();
         if (tid < 32) {
@@ -206,7 +205,7 @@ cudaError_t topk_rows(const float* scores, int64_t rows, int64_t m, int64_t k, i
     const size_t smem = sizeof(uint64_t) * p2 + (stage ? sizeof(float) * m : 0);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_topk_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(k_topk_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 196 * 1024);
         attr_set = true;
     }
     k_topk_rows<<<(unsigned)rows, kTopkThreads, smem, s>>>(scores, m, k, idx, counts, stage, p2);
