@@ -30,6 +30,7 @@
 #ifndef CSD_B200_H
 #define CSD_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -70,6 +71,12 @@ csd_status csd_ctx_destroy(csd_ctx* ctx);
 /* Synchronises `stream` and surfaces in-kernel validation failures
  * (duplicate / out-of-range ids, non-finite logits) as the matching status. */
 csd_status csd_ctx_sync(csd_ctx* ctx, void* stream);
+/* Device memory helpers for hosts that do not link the CUDA runtime themselves (the C++
+ * csd:: mirror).  Synchronous copies on the legacy default stream. */
+csd_status csd_device_alloc(size_t bytes, void** out);
+csd_status csd_device_free(void* ptr);
+csd_status csd_copy_to_device(void* dst, const void* src, size_t bytes);
+csd_status csd_copy_to_host(void* dst, const void* src, size_t bytes);
 /* PROD-mode index-set validation on every sparse call (default on; the block
  * runner disables it for its own top-k sets, which are valid by construction). */
 csd_status csd_ctx_set_validation(csd_ctx* ctx, int enabled);
@@ -133,6 +140,10 @@ csd_status csd_dense_mlp(csd_ctx* ctx, csd_mode mode, const void* x, const void*
                          const float* b1, const void* w2, const float* b2, int64_t batch,
                          int64_t n, int64_t d, int64_t f, int64_t chunk, float* out,
                          void* act_out, void* stream);
+/* MlpDenseResult::preact (mlp.cpp:55-59): pre = x W1^T + b1, [B,N,F] fp32.  CHECK only. */
+csd_status csd_mlp_preact(csd_ctx* ctx, csd_mode mode, const void* x, const void* w1,
+                          const float* b1, int64_t batch, int64_t n, int64_t d, int64_t f,
+                          float* pre_out, void* stream);
 /* mlp_tile_means (mlp.hpp:47, mlp.cpp:83-96): out [B, N/c, F] fp32. */
 csd_status csd_mlp_tile_means(csd_ctx* ctx, csd_mode mode, const void* x, const void* w1,
                               int64_t batch, int64_t n, int64_t d, int64_t f, int64_t chunk,

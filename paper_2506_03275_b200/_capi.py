@@ -42,6 +42,11 @@ SIGNATURES = {
     "csd_ctx_sync": (i32, [p, p]),
     "csd_ctx_launch_count": (i64, [p]),
     "csd_ctx_set_validation": (i32, [p, C.c_int]),
+    "csd_device_alloc": (i32, [C.c_size_t, C.POINTER(p)]),
+    "csd_device_free": (i32, [p]),
+    "csd_copy_to_device": (i32, [p, p, C.c_size_t]),
+    "csd_copy_to_host": (i32, [p, p, C.c_size_t]),
+    "csd_mlp_preact": (i32, [p, i32, fp, fp, fp, i64, i64, i64, i64, fp, p]),
     "csd_voxel_permutation": (i32, [i64] * 6 + [p]),
     "csd_voxel_reorder": (i32, [p, fp, fp] + [i64] * 8 + [C.c_int, p]),
     "csd_select_top_k": (i32, [p, fp, i64, i64, i64, fp, fp, p]),

@@ -83,7 +83,39 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_host(force, verbose)
     return LIB
+
+
+HOST_SRC = os.path.join(PKG, "host", "csd_host.cpp")
+HOST_LIB = os.path.join(PKG, "libcsd_host.so")
+
+
+def _json_include():
+    import site
+    for sp in site.getsitepackages():
+        d = os.path.join(sp, "include", "cudnn_frontend", "thirdparty", "nlohmann")
+        if os.path.exists(os.path.join(d, "json.hpp")):
+            return d
+    raise RuntimeError("nlohmann/json.hpp not found (cudnn_frontend third-party headers)")
+
+
+def build_host(force: bool = False, verbose: bool = False) -> str:
+    """libcsd_host.so: the reference's C++ csd:: API (include/csd/*.hpp) over the C ABI."""
+    deps = [HOST_SRC, LIB] + [os.path.join(INCLUDE, "csd", f)
+                              for f in os.listdir(os.path.join(INCLUDE, "csd"))]
+    if (not force and os.path.exists(HOST_LIB)
+            and os.path.getmtime(HOST_LIB) >= max(os.path.getmtime(p) for p in deps)):
+        return HOST_LIB
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-ffp-contract=off",
+           "-I", INCLUDE, "-I", _json_include(), "-o", HOST_LIB, HOST_SRC,
+           "-L", PKG, "-l:libcsd_b200.so", "-Wl,-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"host library build failed:\n{r.stdout}\n{r.stderr}")
+    return HOST_LIB
 
 
 if __name__ == "__main__":

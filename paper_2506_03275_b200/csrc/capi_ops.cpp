@@ -394,3 +394,39 @@ csd_status csd_add(csd_ctx* ctx, csd_mode mode, const void* a, const void* b, in
 }
 
 }  // extern "C"
+
+extern "C" {
+
+csd_status csd_mlp_preact(csd_ctx* ctx, csd_mode mode, const void* x, const void* w1,
+                          const float* b1, int64_t batch, int64_t n, int64_t d, int64_t f,
+                          float* pre_out, void* stream) {
+    auto* c = reinterpret_cast<Ctx*>(ctx);
+    CSD_TRY(check_mlp_shape(batch, n, d, f));
+    if (mode != CSD_MODE_CHECK)
+        return set_error(CSD_ERR_UNSUPPORTED, "csd_mlp_preact: CHECK mode only");
+    CSD_CU(check_mlp_preact((const float*)x, (const float*)w1, b1, batch * n, d, f, pre_out,
+                            S(stream)), "mlp_preact");
+    c->launches += 1;
+    return CSD_OK;
+}
+
+csd_status csd_device_alloc(size_t bytes, void** out) {
+    if (!out) return set_error(CSD_ERR_VALUE, "csd_device_alloc: null out");
+    *out = nullptr;
+    CSD_CU(cudaMalloc(out, bytes ? bytes : 16), "cudaMalloc");
+    return CSD_OK;
+}
+csd_status csd_device_free(void* ptr) {
+    if (ptr) CSD_CU(cudaFree(ptr), "cudaFree");
+    return CSD_OK;
+}
+csd_status csd_copy_to_device(void* dst, const void* src, size_t bytes) {
+    if (bytes) CSD_CU(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "cudaMemcpy h2d");
+    return CSD_OK;
+}
+csd_status csd_copy_to_host(void* dst, const void* src, size_t bytes) {
+    if (bytes) CSD_CU(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "cudaMemcpy d2h");
+    return CSD_OK;
+}
+
+}  // extern "C"

@@ -424,3 +424,17 @@ cudaError_t check_sparse_delta_mlp(const float* x, const float* w1, const float*
 
 }  // namespace dev
 }  // namespace csd
+
+namespace csd {
+namespace dev {
+// pre = x W1^T + b1 (mlp.cpp:55-59), the MlpDenseResult::preact view.
+cudaError_t check_mlp_preact(const float* x, const float* w1, const float* b1, int64_t rows,
+                             int64_t d, int64_t f, float* pre, cudaStream_t s) {
+    ExactGemm p{};
+    p.a = x; p.lda = d; p.b = w1; p.ldb = d; p.trans_b = true;
+    p.c = pre; p.ldc = f; p.M = rows; p.N = f; p.K = d; p.inner = 1;
+    p.epi = 2; p.bias = b1;
+    return launch_exact(p, 1, s);
+}
+}  // namespace dev
+}  // namespace csd

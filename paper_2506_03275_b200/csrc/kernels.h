@@ -36,6 +36,8 @@ cudaError_t check_add(const float* a, const float* b, int64_t numel, float* out,
 cudaError_t check_dense_mlp(const float* x, const float* w1, const float* b1, const float* w2,
                             const float* b2, int64_t batch, int64_t n, int64_t d, int64_t f,
                             float* act_ref, float* out, cudaStream_t s);
+cudaError_t check_mlp_preact(const float* x, const float* w1, const float* b1, int64_t rows,
+                             int64_t d, int64_t f, float* pre, cudaStream_t s);
 cudaError_t check_tile_means(const float* x, const float* w1, int64_t batch, int64_t n, int64_t d,
                              int64_t f, int64_t chunk, float* means_ws, float* out,
                              cudaStream_t s);

@@ -1,0 +1,558 @@
+// csd_host.cpp — the reference's C++ csd:: operator API (include/csd/*.hpp) implemented on
+// top of the C ABI (include/csd_b200.h).  A caller of the reference library relinks against
+// libcsd_host.so and its voxel / top-k / attention / MLP calls run on the B200 in
+// CSD_MODE_CHECK (bit-exact with the reference's CPU arithmetic); the caches keep the
+// reference's public host layouts so existing callers and tests read them unchanged.
+//
+// Validation order and exception types follow the reference functions cited per routine;
+// the ABI's csd_status codes are rethrown as the matching csd:: exception.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include <json.hpp>
+
+#include "csd/attention.hpp"
+#include "csd/metrics.hpp"
+#include "csd/mlp.hpp"
+#include "csd/voxel.hpp"
+#include "csd_b200.h"
+
+namespace csd {
+namespace {
+
+[[noreturn]] void rethrow(csd_status s) {
+    const std::string msg = csd_last_error();
+    switch (s) {
+        case CSD_ERR_SHAPE: throw ShapeError(msg);
+        case CSD_ERR_INDEX: throw IndexError(msg);
+        case CSD_ERR_NUMERIC: throw NumericError(msg);
+        case CSD_ERR_STATE: throw StateError(msg);
+        case CSD_ERR_VALUE: throw ValueError(msg);
+        case CSD_ERR_CONFIG: throw ConfigError(msg);
+        default: throw Error(std::string(csd_status_name(s)) + ": " + msg);
+    }
+}
+void ok(csd_status s) {
+    if (s != CSD_OK) rethrow(s);
+}
+
+csd_ctx* ctx() {  // one context per process, on device 0 (fails loudly without a GPU)
+    static csd_ctx* c = [] {
+        csd_ctx* h = nullptr;
+        ok(csd_ctx_create(0, &h));
+        return h;
+    }();
+    return c;
+}
+
+// RAII device buffer
+class Dev {
+public:
+    explicit Dev(size_t bytes) : bytes_(bytes) { ok(csd_device_alloc(bytes, &p_)); }
+    template <class T>
+    explicit Dev(const std::vector<T>& host) : Dev(host.size() * sizeof(T)) {
+        ok(csd_copy_to_device(p_, host.data(), bytes_));
+    }
+    explicit Dev(const Tensor& t) : Dev(sizeof(float) * static_cast<size_t>(t.numel())) {
+        ok(csd_copy_to_device(p_, t.data(), bytes_));
+    }
+    ~Dev() { csd_device_free(p_); }
+    Dev(const Dev&) = delete;
+    Dev& operator=(const Dev&) = delete;
+    float* f() const { return static_cast<float*>(p_); }
+    int32_t* i() const { return static_cast<int32_t*>(p_); }
+    void* v() const { return p_; }
+    void to(Tensor& t) const { ok(csd_copy_to_host(t.data(), p_, sizeof(float) * t.numel())); }
+    template <class T>
+    void to(std::vector<T>& h) const { ok(csd_copy_to_host(h.data(), p_, sizeof(T) * h.size())); }
+
+private:
+    void* p_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+void sync() { ok(csd_ctx_sync(ctx(), nullptr)); }
+
+}  // namespace
+
+// ====================================================================== Tensor (host)
+Tensor::Tensor() : dims_(), vals_(1, 0.0f) {}
+Tensor::Tensor(std::vector<int64_t> shape) : dims_(std::move(shape)) {
+    for (int64_t d : dims_)
+        if (d < 1) throw ShapeError("invalid tensor shape " + shape_str(dims_) + ": dims must be >= 1");
+    vals_.assign(static_cast<size_t>(shape_numel(dims_)), 0.0f);
+}
+Tensor::Tensor(std::vector<int64_t> shape, std::vector<float> data)
+    : dims_(std::move(shape)), vals_(std::move(data)) {
+    for (int64_t d : dims_)
+        if (d < 1) throw ShapeError("invalid tensor shape " + shape_str(dims_) + ": dims must be >= 1");
+    if (shape_numel(dims_) != static_cast<int64_t>(vals_.size()))
+        throw ShapeError("tensor data length " + std::to_string(vals_.size()) +
+                         " does not match shape " + shape_str(dims_));
+}
+Tensor Tensor::full(std::vector<int64_t> shape, float value) {
+    Tensor t(std::move(shape));
+    std::fill(t.vals_.begin(), t.vals_.end(), value);
+    return t;
+}
+int64_t Tensor::dim(int64_t axis) const {
+    if (axis < 0 || axis >= rank())
+        throw ShapeError("dimension index " + std::to_string(axis) + " out of range for shape " +
+                         shape_str(dims_));
+    return dims_[static_cast<size_t>(axis)];
+}
+std::string shape_str(const std::vector<int64_t>& shape) {
+    std::string s = "[";
+    for (size_t i = 0; i < shape.size(); ++i) s += (i ? "x" : "") + std::to_string(shape[i]);
+    return s + "]";
+}
+int64_t shape_numel(const std::vector<int64_t>& shape) {
+    int64_t n = 1;
+    for (int64_t d : shape) n *= d;
+    return n;
+}
+
+// Host tensor utilities with the reference's arithmetic (tensor.cpp:66-225): sequential
+// fp32 accumulation (this file is compiled with -ffp-contract=off).
+Tensor gemm(const Tensor& a, const Tensor& b, bool transpose_b) {
+    if (a.rank() != 2 || b.rank() != 2)
+        throw ShapeError("gemm expects rank-2 operands, got " + shape_str(a.shape()) + " and " +
+                         shape_str(b.shape()));
+    const int64_t m = a.dim(0), kk = a.dim(1);
+    const int64_t inner = transpose_b ? b.dim(1) : b.dim(0), n = transpose_b ? b.dim(0) : b.dim(1);
+    if (kk != inner)
+        throw ShapeError("gemm inner dimensions disagree: " + shape_str(a.shape()) + " @ " +
+                         shape_str(b.shape()));
+    Tensor c({m, n});
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+            float acc = 0.0f;
+            for (int64_t k = 0; k < kk; ++k)
+                acc += a[i * kk + k] * (transpose_b ? b[j * kk + k] : b[k * n + j]);
+            c[i * n + j] = acc;
+        }
+    return c;
+}
+SoftmaxResult softmax_rows(const Tensor& logits) {
+    if (logits.rank() < 1) throw ShapeError("softmax_rows expects rank >= 1, got scalar");
+    const int64_t len = logits.dim(logits.rank() - 1), rows = logits.numel() / len;
+    std::vector<int64_t> st(logits.shape().begin(), logits.shape().end() - 1);
+    SoftmaxResult r{Tensor(logits.shape()), {Tensor(st), Tensor(st)}};
+    for (int64_t i = 0; i < rows; ++i) {
+        const float* row = logits.data() + i * len;
+        float m = row[0];
+        for (int64_t j = 0; j < len; ++j) {
+            if (!std::isfinite(row[j]))
+                throw NumericError("softmax_rows: non-finite logit at row " + std::to_string(i) +
+                                   ", position " + std::to_string(j));
+            m = std::max(m, row[j]);
+        }
+        float l = 0.0f;
+        float* o = r.probs.data() + i * len;
+        for (int64_t j = 0; j < len; ++j) l += (o[j] = std::exp(row[j] - m));
+        for (int64_t j = 0; j < len; ++j) o[j] /= l;
+        r.stats.row_max[i] = m;
+        r.stats.exp_sum[i] = l;
+    }
+    return r;
+}
+Tensor gelu(const Tensor& x) {
+    const float k = std::sqrt(2.0f / static_cast<float>(M_PI));
+    Tensor y(x.shape());
+    for (int64_t i = 0; i < x.numel(); ++i) {
+        const float v = x[i];
+        y[i] = 0.5f * v * (1.0f + std::tanh(k * (v + 0.044715f * v * v * v)));
+    }
+    return y;
+}
+Tensor gather_rows(const Tensor& t, const std::vector<int64_t>& indices) {
+    if (t.rank() < 2) throw ShapeError("gather_rows expects rank >= 2, got " + shape_str(t.shape()));
+    const int64_t cols = t.dim(t.rank() - 1), rows = t.dim(t.rank() - 2);
+    for (int64_t id : indices)
+        if (id < 0 || id >= rows)
+            throw IndexError("gather_rows: index " + std::to_string(id) + " out of range [0, " +
+                             std::to_string(rows) + ")");
+    if (indices.empty()) throw ShapeError("gather_rows: empty index list");
+    std::vector<int64_t> os = t.shape();
+    os[os.size() - 2] = static_cast<int64_t>(indices.size());
+    Tensor out(os);
+    const int64_t slices = t.numel() / (rows * cols), orow = static_cast<int64_t>(indices.size());
+    for (int64_t s = 0; s < slices; ++s)
+        for (int64_t j = 0; j < orow; ++j)
+            std::memcpy(out.data() + (s * orow + j) * cols,
+                        t.data() + (s * rows + indices[static_cast<size_t>(j)]) * cols,
+                        sizeof(float) * cols);
+    return out;
+}
+Tensor chunk_reduce(const Tensor& t, int64_t chunk, ReduceMode mode) {
+    if (t.rank() < 2) throw ShapeError("chunk_reduce expects rank >= 2, got " + shape_str(t.shape()));
+    if (chunk < 1) throw ValueError("chunk_reduce: chunk must be >= 1, got " + std::to_string(chunk));
+    const int64_t cols = t.dim(t.rank() - 1), rows = t.dim(t.rank() - 2);
+    if (rows % chunk)
+        throw ShapeError("chunk_reduce: row count " + std::to_string(rows) +
+                         " not divisible by chunk " + std::to_string(chunk));
+    std::vector<int64_t> os = t.shape();
+    os[os.size() - 2] = rows / chunk;
+    Tensor out(os);
+    const int64_t slices = t.numel() / (rows * cols);
+    const float inv = 1.0f / static_cast<float>(chunk);
+    for (int64_t s = 0; s < slices; ++s)
+        for (int64_t i = 0; i < rows / chunk; ++i) {
+            float* w = out.data() + (s * (rows / chunk) + i) * cols;
+            for (int64_t r = i * chunk; r < (i + 1) * chunk; ++r)
+                for (int64_t c = 0; c < cols; ++c) w[c] += t[(s * rows + r) * cols + c];
+            if (mode == ReduceMode::Mean)
+                for (int64_t c = 0; c < cols; ++c) w[c] *= inv;
+        }
+    return out;
+}
+double r_squared(const Tensor& exact, const Tensor& approx) {
+    if (exact.shape() != approx.shape())
+        throw ShapeError("r_squared shapes disagree: " + shape_str(exact.shape()) + " vs " +
+                         shape_str(approx.shape()));
+    const int64_t n = exact.numel();
+    double mean = 0.0;
+    for (int64_t i = 0; i < n; ++i) mean += exact[i];
+    mean /= static_cast<double>(n);
+    double res = 0.0, tot = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        const double e = exact[i], a = approx[i];
+        res += (e - a) * (e - a);
+        tot += (e - mean) * (e - mean);
+    }
+    if (tot == 0.0) throw NumericError("r_squared undefined: true delta has zero variance");
+    return 1.0 - res / tot;
+}
+
+// ====================================================================== voxel (device)
+void VoxelLayout::validate() const {  // voxel.cpp:7-16
+    if (t < 1 || h < 1 || w < 1 || vt < 1 || vh < 1 || vw < 1)
+        throw ConfigError("voxel layout dimensions must be >= 1");
+    if (t % vt || h % vh || w % vw)
+        throw ConfigError("voxel (" + std::to_string(vt) + "," + std::to_string(vh) + "," +
+                          std::to_string(vw) + ") does not tile grid (" + std::to_string(t) + "," +
+                          std::to_string(h) + "," + std::to_string(w) + ")");
+}
+std::vector<int64_t> voxel_permutation(const VoxelLayout& L) {
+    L.validate();
+    std::vector<int64_t> perm(static_cast<size_t>(L.tokens()));
+    ok(csd_voxel_permutation(L.t, L.h, L.w, L.vt, L.vh, L.vw, perm.data()));
+    return perm;
+}
+VoxelOrderResult voxel_order(const Tensor& x, const VoxelLayout& L) {  // voxel.cpp:44-73
+    L.validate();
+    if (x.rank() != 5) throw ShapeError("voxel_order expects [B x T x H x W x D], got " + shape_str(x.shape()));
+    if (x.dim(1) != L.t || x.dim(2) != L.h || x.dim(3) != L.w)
+        throw ShapeError("voxel_order: tensor grid " + shape_str(x.shape()) + " does not match layout");
+    VoxelOrderResult r{Tensor({x.dim(0), L.tokens(), x.dim(4)}), voxel_permutation(L)};
+    Dev src(x), dst(sizeof(float) * x.numel());
+    ok(csd_voxel_reorder(ctx(), src.v(), dst.v(), x.dim(0), L.t, L.h, L.w, L.vt, L.vh, L.vw,
+                         sizeof(float) * x.dim(4), 0, nullptr));
+    dst.to(r.reordered);
+    return r;
+}
+Tensor reverse_voxel_order(const Tensor& x, const VoxelLayout& L) {  // voxel.cpp:75-102
+    L.validate();
+    if (x.rank() != 3) throw ShapeError("reverse_voxel_order expects [B x N x D], got " + shape_str(x.shape()));
+    if (x.dim(1) != L.tokens())
+        throw ShapeError("reverse_voxel_order: sequence length " + std::to_string(x.dim(1)) +
+                         " does not match layout token count " + std::to_string(L.tokens()));
+    Tensor out({x.dim(0), L.t, L.h, L.w, x.dim(2)});
+    Dev src(x), dst(sizeof(float) * x.numel());
+    ok(csd_voxel_reorder(ctx(), src.v(), dst.v(), x.dim(0), L.t, L.h, L.w, L.vt, L.vh, L.vw,
+                         sizeof(float) * x.dim(2), 1, nullptr));
+    dst.to(out);
+    return out;
+}
+
+// ====================================================================== index sets
+SparseIndexSet SparseIndexSet::empty(int64_t batch, int64_t heads, int64_t chunks,
+                                     int64_t chunk_size, int64_t k_max, int64_t domain) {
+    SparseIndexSet s;
+    s.batch = batch; s.heads = heads; s.chunks = chunks; s.chunk_size = chunk_size;
+    s.k_max = k_max; s.domain = domain;
+    s.indices.assign(static_cast<size_t>(batch * heads * chunks * k_max), 0);
+    s.counts.assign(static_cast<size_t>(batch * heads * chunks), 0);
+    return s;
+}
+void SparseIndexSet::validate() const {  // sparse_index.cpp:27-62, range/dup checks on device
+    if (batch < 1 || heads < 1 || chunks < 1 || chunk_size < 1 || domain < 1)
+        throw ValueError("sparse index set has empty dimensions");
+    if (k_max < 0 || k_max > domain)
+        throw ValueError("sparse index set k_max " + std::to_string(k_max) + " outside [0, domain=" +
+                         std::to_string(domain) + "]");
+    if (static_cast<int64_t>(indices.size()) != batch * heads * chunks * k_max ||
+        static_cast<int64_t>(counts.size()) != batch * heads * chunks)
+        throw ValueError("sparse index set storage does not match its dimensions");
+    Dev di(indices.empty() ? std::vector<int32_t>{0} : indices), dc(counts);
+    ok(csd_validate_index_set(ctx(), di.i(), dc.i(), batch * heads * chunks, k_max, domain, nullptr));
+    sync();
+}
+SparseIndexSet select_top_k(const Tensor& scores, int64_t k, int64_t chunk_size) {
+    if (scores.rank() != 4)
+        throw ShapeError("select_top_k expects [B x H x C x M] scores, got " + shape_str(scores.shape()));
+    const int64_t b = scores.dim(0), h = scores.dim(1), c = scores.dim(2), m = scores.dim(3);
+    if (k < 1 || k > m)
+        throw ValueError("select_top_k: k=" + std::to_string(k) + " outside [1, " + std::to_string(m) + "]");
+    SparseIndexSet s = SparseIndexSet::empty(b, h, c, chunk_size, k, m);
+    Dev ds(scores), di(sizeof(int32_t) * s.indices.size()), dc(sizeof(int32_t) * s.counts.size());
+    ok(csd_select_top_k(ctx(), ds.f(), b * h * c, m, k, di.i(), dc.i(), nullptr));
+    di.to(s.indices);
+    dc.to(s.counts);
+    return s;
+}
+SparseIndexSet load_index_set_json(const std::string& text, int64_t batch, int64_t heads,
+                                   int64_t chunks, int64_t domain) {  // sparse_index.cpp:98-148
+    nlohmann::json doc;
+    try {
+        doc = nlohmann::json::parse(text);
+    } catch (const nlohmann::json::exception& e) {
+        throw IoError(std::string("sparsity pattern JSON parse failure: ") + e.what());
+    }
+    if (!doc.is_object() || !doc.contains("chunk_size") || !doc.contains("k_max") || !doc.contains("entries"))
+        throw IoError("sparsity pattern JSON must contain chunk_size, k_max, entries");
+    const int64_t k_max = doc["k_max"].get<int64_t>();
+    if (k_max < 1 || k_max > domain)
+        throw ValueError("sparsity pattern k_max " + std::to_string(k_max) + " outside [1, " +
+                         std::to_string(domain) + "]");
+    SparseIndexSet s = SparseIndexSet::empty(batch, heads, chunks, doc["chunk_size"].get<int64_t>(),
+                                             k_max, domain);
+    for (const auto& e : doc["entries"]) {
+        if (!e.is_array() || e.size() != 4) throw IoError("sparsity pattern entry must be [b, h, chunk, [ids...]]");
+        const int64_t b = e[0].get<int64_t>(), h = e[1].get<int64_t>(), c = e[2].get<int64_t>();
+        if (b < 0 || b >= batch || h < 0 || h >= heads || c < 0 || c >= chunks) {
+            std::ostringstream os;
+            os << "sparsity pattern entry (" << b << "," << h << "," << c << ") outside dims ("
+               << batch << "," << heads << "," << chunks << ")";
+            throw IndexError(os.str());
+        }
+        if (static_cast<int64_t>(e[3].size()) > k_max)
+            throw ValueError("sparsity pattern entry lists more than k_max ids");
+        int32_t* dst = s.chunk_indices(b, h, c);
+        int32_t n = 0;
+        for (const auto& v : e[3]) {
+            const int64_t id = v.get<int64_t>();
+            if (id < 0 || id >= domain)
+                throw IndexError("sparsity pattern index " + std::to_string(id) + " out of range [0, " +
+                                 std::to_string(domain) + ")");
+            dst[n++] = static_cast<int32_t>(id);
+        }
+        s.counts[static_cast<size_t>((b * heads + h) * chunks + c)] = n;
+    }
+    s.validate();
+    return s;
+}
+SparseIndexSet load_index_set_json_file(const std::string& path, int64_t batch, int64_t heads,
+                                        int64_t chunks, int64_t domain) {
+    std::ifstream f(path);
+    if (!f) throw IoError("cannot open " + path + " for reading");
+    std::stringstream buf;
+    buf << f.rdbuf();
+    return load_index_set_json(buf.str(), batch, heads, chunks, domain);
+}
+
+// ====================================================================== attention (device)
+namespace {
+void check_qkv(const Tensor& q, const Tensor& k, const Tensor& v) {  // attention.cpp:11-21
+    if (q.rank() != 4 || k.rank() != 4 || v.rank() != 4)
+        throw ShapeError("attention expects [B x H x N x E] tensors, got q=" + shape_str(q.shape()) +
+                         " k=" + shape_str(k.shape()) + " v=" + shape_str(v.shape()));
+    if (q.shape() != k.shape() || q.shape() != v.shape())
+        throw ShapeError("attention q/k/v shapes disagree: q=" + shape_str(q.shape()) + " k=" +
+                         shape_str(k.shape()) + " v=" + shape_str(v.shape()));
+}
+void check_index_set(const SparseIndexSet& idx, const Tensor& q) {  // attention.cpp:46-55
+    if (idx.batch != q.dim(0) || idx.heads != q.dim(1))
+        throw ShapeError("sparse index set dims do not match q " + shape_str(q.shape()));
+    if (idx.domain != q.dim(2) || idx.chunks * idx.chunk_size != q.dim(2))
+        throw ShapeError("sparse index set chunking does not cover the sequence length " +
+                         std::to_string(q.dim(2)));
+}
+}  // namespace
+
+Tensor dense_attention(const Tensor& q, const Tensor& k, const Tensor& v) {
+    check_qkv(q, k, v);
+    Tensor out(q.shape());
+    Dev dq(q), dk(k), dv(v), dout(sizeof(float) * q.numel());
+    ok(csd_dense_attention(ctx(), CSD_MODE_CHECK, CSD_LAYOUT_BHNE, dq.v(), dk.v(), dv.v(), q.dim(0),
+                           q.dim(1), q.dim(2), q.dim(3), dout.v(), nullptr));
+    dout.to(out);
+    return out;
+}
+ColumnSumAttentionResult column_sum_attention(const Tensor& q, const Tensor& k, const Tensor& v,
+                                              const SoftmaxStats* prev, int64_t chunk) {
+    check_qkv(q, k, v);
+    const int64_t b = q.dim(0), h = q.dim(1), n = q.dim(2), e = q.dim(3);
+    if (chunk < 1 || n % chunk)
+        throw ShapeError("column_sum_attention: sequence length " + std::to_string(n) +
+                         " not divisible by chunk " + std::to_string(chunk));
+    if (prev && (prev->row_max.shape() != std::vector<int64_t>{b, h, n} ||
+                 prev->exp_sum.shape() != std::vector<int64_t>{b, h, n}))
+        throw ShapeError("column_sum_attention: previous stats shape " +
+                         shape_str(prev->row_max.shape()) + " does not match");
+    ColumnSumAttentionResult r{Tensor(q.shape()), Tensor({b, h, n / chunk, n}),
+                               {Tensor({b, h, n}), Tensor({b, h, n})}};
+    Dev dq(q), dk(k), dv(v), dout(sizeof(float) * q.numel()), dm(sizeof(float) * b * h * n),
+        dl(sizeof(float) * b * h * n), dcs(sizeof(float) * r.column_sums.numel());
+    Dev pm(prev ? prev->row_max : Tensor({1})), pl(prev ? prev->exp_sum : Tensor({1}));
+    ok(csd_column_sum_attention(ctx(), CSD_MODE_CHECK, CSD_LAYOUT_BHNE, dq.v(), dk.v(), dv.v(),
+                                prev ? pm.f() : nullptr, prev ? pl.f() : nullptr, b, h, n, e, chunk,
+                                dout.v(), dm.f(), dl.f(), dcs.f(), nullptr));
+    dout.to(r.output);
+    dcs.to(r.column_sums);
+    dm.to(r.stats.row_max);
+    dl.to(r.stats.exp_sum);
+    return r;
+}
+Tensor sparse_delta_attention(const Tensor& q, const Tensor& k, const Tensor& v,
+                              const SparseIndexSet& idx, const Tensor& base, float scale) {
+    check_qkv(q, k, v);
+    if (base.shape() != q.shape())
+        throw ShapeError("sparse_delta_attention: base shape " + shape_str(base.shape()) +
+                         " does not match q " + shape_str(q.shape()));
+    check_index_set(idx, q);
+    Tensor out(q.shape());
+    Dev dq(q), dk(k), dv(v), db(base), dout(sizeof(float) * q.numel());
+    Dev di(idx.indices.empty() ? std::vector<int32_t>{0} : idx.indices), dc(idx.counts);
+    ok(csd_sparse_delta_attention(ctx(), CSD_MODE_CHECK, CSD_LAYOUT_BHNE, dq.v(), dk.v(), dv.v(),
+                                  di.i(), dc.i(), idx.k_max, idx.chunk_size, db.v(), scale,
+                                  q.dim(0), q.dim(1), q.dim(2), q.dim(3), dout.v(), nullptr));
+    dout.to(out);
+    return out;
+}
+Tensor attention_step(const Tensor& q, const Tensor& k, const Tensor& v, AttentionCache& cache,
+                      bool dense_step, int64_t top_k, int64_t chunk,
+                      const SparseIndexSet* static_indices) {  // attention.cpp:196-219
+    if (!dense_step && !cache.initialized)
+        throw StateError("sparse attention step requested before any dense step");
+    if (dense_step) {
+        auto res = column_sum_attention(q, k, v, cache.initialized ? &cache.stats : nullptr, chunk);
+        SparseIndexSet idx = static_indices ? *static_indices : select_top_k(res.column_sums, top_k, chunk);
+        check_index_set(idx, q);
+        idx.validate();
+        cache.residual_output = sparse_delta_attention(q, k, v, idx, res.output, -1.0f);
+        cache.stats = std::move(res.stats);
+        cache.indices = std::move(idx);
+        cache.age = 0;
+        cache.initialized = true;
+        return res.output;
+    }
+    cache.age += 1;
+    return sparse_delta_attention(q, k, v, cache.indices, cache.residual_output, 1.0f);
+}
+
+// ====================================================================== MLP (device)
+void MlpWeights::validate() const {  // mlp.cpp:38-47
+    if (w1.rank() != 2 || w2.rank() != 2 || b1.rank() != 1 || b2.rank() != 1)
+        throw ShapeError("mlp weights must be w1 [F x D], b1 [F], w2 [F x D], b2 [D]");
+    if (w2.shape() != w1.shape() || b1.dim(0) != w1.dim(0) || b2.dim(0) != w1.dim(1))
+        throw ShapeError("mlp weight shapes disagree: w1=" + shape_str(w1.shape()) + " w2=" +
+                         shape_str(w2.shape()));
+}
+namespace {
+void check_x(const Tensor& x, const MlpWeights& w) {  // mlp.cpp:26-34
+    if (x.rank() != 3) throw ShapeError("mlp expects [B x N x D] input, got " + shape_str(x.shape()));
+    if (x.dim(2) != w.model_dim())
+        throw ShapeError("mlp input dim " + std::to_string(x.dim(2)) +
+                         " does not match weights' model dim " + std::to_string(w.model_dim()));
+}
+}  // namespace
+
+MlpDenseResult dense_mlp(const Tensor& x, const MlpWeights& w) {
+    w.validate();
+    check_x(x, w);
+    const int64_t b = x.dim(0), n = x.dim(1), d = x.dim(2), f = w.hidden();
+    MlpDenseResult r{Tensor({b, n, d}), Tensor({b, n, f}), Tensor({b, n, f})};
+    Dev dx(x), d1(w.w1), db1(w.b1), d2(w.w2), db2(w.b2), dout(sizeof(float) * b * n * d),
+        dact(sizeof(float) * b * n * f), dpre(sizeof(float) * b * n * f);
+    ok(csd_dense_mlp(ctx(), CSD_MODE_CHECK, dx.v(), d1.v(), db1.f(), d2.v(), db2.f(), b, n, d, f, n,
+                     dout.f(), dact.v(), nullptr));
+    ok(csd_mlp_preact(ctx(), CSD_MODE_CHECK, dx.v(), d1.v(), db1.f(), b, n, d, f, dpre.f(), nullptr));
+    dout.to(r.output);
+    dact.to(r.act);
+    dpre.to(r.preact);
+    return r;
+}
+Tensor mlp_tile_means(const Tensor& x, const Tensor& w1, int64_t chunk) {
+    if (x.rank() != 3) throw ShapeError("mlp_tile_means expects [B x N x D] input, got " + shape_str(x.shape()));
+    if (w1.rank() != 2 || w1.dim(1) != x.dim(2))
+        throw ShapeError("gemm inner dimensions disagree: " + shape_str(x.shape()) + " @ " +
+                         shape_str(w1.shape()) + " (b transposed)");
+    const int64_t b = x.dim(0), n = x.dim(1), d = x.dim(2), f = w1.dim(0);
+    if (chunk < 1 || n % chunk)
+        throw ShapeError("chunk_reduce: row count " + std::to_string(n) + " not divisible by chunk " +
+                         std::to_string(chunk));
+    Tensor out({b, n / chunk, f});
+    Dev dx(x), d1(w1), dout(sizeof(float) * out.numel());
+    ok(csd_mlp_tile_means(ctx(), CSD_MODE_CHECK, dx.v(), d1.v(), b, n, d, f, chunk, dout.f(), nullptr));
+    dout.to(out);
+    return out;
+}
+SparseIndexSet mlp_change_indices(const Tensor& x, const Tensor& w1, const Tensor& tile_means,
+                                  int64_t k, int64_t chunk) {  // mlp.cpp:98-118
+    if (x.rank() != 3) throw ShapeError("mlp_tile_means expects [B x N x D] input, got " + shape_str(x.shape()));
+    const int64_t b = x.dim(0), n = x.dim(1), d = x.dim(2), f = w1.dim(0);
+    if (chunk < 1 || n % chunk)
+        throw ShapeError("chunk_reduce: row count " + std::to_string(n) + " not divisible by chunk " +
+                         std::to_string(chunk));
+    if (tile_means.shape() != std::vector<int64_t>{b, n / chunk, f})
+        throw ShapeError("mlp_change_indices: cached tile means " + shape_str(tile_means.shape()) +
+                         " do not match fresh");
+    if (k < 1 || k > f)
+        throw ValueError("mlp_change_indices: k=" + std::to_string(k) + " outside [1, " + std::to_string(f) + "]");
+    SparseIndexSet s = SparseIndexSet::empty(b, 1, n / chunk, chunk, k, f);
+    Dev dx(x), d1(w1), dtm(tile_means), di(sizeof(int32_t) * s.indices.size()),
+        dc(sizeof(int32_t) * s.counts.size());
+    ok(csd_mlp_change_indices(ctx(), CSD_MODE_CHECK, dx.v(), d1.v(), dtm.f(), b, n, d, f, k, chunk,
+                              di.i(), dc.i(), nullptr));
+    di.to(s.indices);
+    dc.to(s.counts);
+    return s;
+}
+Tensor sparse_delta_mlp(const Tensor& x, const MlpWeights& w, const SparseIndexSet& idx,
+                        MlpCache& cache) {  // mlp.cpp:120-182
+    w.validate();
+    check_x(x, w);
+    if (!cache.initialized) throw StateError("sparse MLP step requested before any dense step");
+    const int64_t b = x.dim(0), n = x.dim(1), d = x.dim(2), f = w.hidden();
+    if (idx.batch != b || idx.heads != 1 || idx.domain != f || idx.chunks * idx.chunk_size != n)
+        throw ShapeError("mlp sparse index set does not match (B=" + std::to_string(b) + ", N=" +
+                         std::to_string(n) + ", F=" + std::to_string(f) + ")");
+    Dev dx(x), d1(w.w1), db1(w.b1), d2(w.w2), dact(cache.activations), dout(cache.outputs);
+    Dev di(idx.indices.empty() ? std::vector<int32_t>{0} : idx.indices), dc(idx.counts);
+    ok(csd_sparse_delta_mlp(ctx(), CSD_MODE_CHECK, dx.v(), d1.v(), db1.f(), d2.v(), di.i(), dc.i(),
+                            idx.k_max, idx.chunk_size, b, n, d, f, dact.v(), dout.f(), nullptr));
+    dact.to(cache.activations);
+    dout.to(cache.outputs);
+    return cache.outputs;
+}
+Tensor mlp_step(const Tensor& x, const MlpWeights& w, MlpCache& cache, bool dense_step,
+                int64_t top_k, int64_t chunk) {  // mlp.cpp:184-211
+    if (!dense_step && !cache.initialized) throw StateError("sparse MLP step requested before any dense step");
+    if (x.rank() != 3) throw ShapeError("mlp_step expects [B x N x D] input, got " + shape_str(x.shape()));
+    if (chunk < 1 || x.dim(1) % chunk)
+        throw ShapeError("mlp_step: sequence length " + std::to_string(x.dim(1)) +
+                         " not divisible by chunk " + std::to_string(chunk));
+    if (dense_step) {
+        auto res = dense_mlp(x, w);
+        cache.tile_means = mlp_tile_means(x, w.w1, chunk);
+        cache.activations = std::move(res.act);
+        cache.outputs = res.output;
+        cache.indices = SparseIndexSet{};
+        cache.age = 0;
+        cache.initialized = true;
+        return res.output;
+    }
+    SparseIndexSet idx = mlp_change_indices(x, w.w1, cache.tile_means, top_k, chunk);
+    cache.age += 1;
+    Tensor out = sparse_delta_mlp(x, w, idx, cache);
+    cache.indices = std::move(idx);
+    return out;
+}
+
+}  // namespace csd
