@@ -31,30 +31,6 @@ __device__ __forceinline__ uint32_t ord_key(float x) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-// Block-wide exclusive scan of a 0/1 flag in index order; returns the
-// thread's rank and writes the block total to *total.
-__device__ __forceinline__ uint32_t block_rank(bool flag, uint32_t* warp_tot, uint32_t* total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t ballot = __ballot_sync(0xffffffffu, flag);
-    const uint32_t in_warp = __popc(ballot & ((1u << lane) - 1u));
-    if (lane == 0) warp_tot[warp] = __popc(ballot);
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t v = lane < kTopkWarps ? warp_tot[lane] : 0u;
-        uint32_t incl = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane < kTopkWarps) warp_tot[lane] = incl - v;  // exclusive
-        if (lane == 31) *total = incl;
-    }
-    __syncthreads();
-    const uint32_t r = warp_tot[warp] + in_warp;
-    __syncthreads();
-    return r;
-}
-
 __global__ void __launch_bounds__(kTopkThreads)
 k_topk_rows(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* __restrict__ idx_out,
             int32_t* __restrict__ counts, int stage_row, int sort_pow2) {
@@ -125,25 +101,57 @@ k_topk_rows(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* __r
     const uint32_t need_eq = s_kleft;           // ties to take, lowest index first
     const uint32_t G = (uint32_t)k - need_eq;   // strictly greater
 
-    uint32_t eq_base = 0;
-    for (int64_t j0 = 0; j0 < m; j0 += kTopkThreads) {
-        const int64_t j = j0 + tid;
+    // collect: warp w owns the contiguous segment [w*seg, (w+1)*seg); one counting pass,
+    // one block scan of the per-warp tie counts (index order = warp order), one write pass
+    const int lane = tid & 31;
+    const int64_t seg = ((m + kTopkWarps * 32 - 1) / (kTopkWarps * 32)) * 32;
+    const int64_t s0 = warp_id * seg, s1 = min(m, s0 + seg);
+    uint32_t n_eq = 0;
+    for (int64_t j0 = s0; j0 < s1; j0 += 32) {
+        const int64_t j = j0 + lane;
+        n_eq += __popc(__ballot_sync(0xffffffffu, j < s1 && ord_key(src[j]) == T));
+    }
+    if (lane == 0) warp_tot[warp_id] = n_eq;
+    __syncthreads();
+    if (tid < 32) {
+        const uint32_t v = tid < kTopkWarps ? warp_tot[tid] : 0u;
+        uint32_t incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (tid >= o) incl += t;
+        }
+        if (tid < kTopkWarps) warp_tot[tid] = incl - v;  // exclusive tie offset per warp
+    }
+    __syncthreads();
+    uint32_t eq_run = warp_tot[warp_id];
+    for (int64_t j0 = s0; j0 < s1; j0 += 32) {
+        const int64_t j = j0 + lane;
         uint32_t o = 0;
-        bool gt = false, eq = false;
-        if (j < m) {
-            o = ord_key(src[j]);
-            gt = o > T;
-            eq = o == T;
+        if (j < s1) o = ord_key(src[j]);
+        const bool gt = j < s1 && o > T, eq = j < s1 && o == T;
+        const uint64_t comp = ((uint64_t)o << 32) | (uint32_t)~(uint32_t)j;
+        const uint32_t gb = __ballot_sync(0xffffffffu, gt);
+        uint32_t gbase = 0;
+        if (lane == 0 && gb) gbase = atomicAdd(&s_gt, (uint32_t)__popc(gb));
+        gbase = __shfl_sync(0xffffffffu, gbase, 0);
+        if (gt) sel[gbase + __popc(gb & ((1u << lane) - 1u))] = comp;
+        const uint32_t eb = __ballot_sync(0xffffffffu, eq);
+        const uint32_t r = eq_run + __popc(eb & ((1u << lane) - 1u));
+        if (eq && r < need_eq) sel[G + r] = comp;
+        eq_run += __popc(eb);
+    }
+    __syncthreads();
+    int32_t* dst = idx_out + row * k;
+    if (k <= 2048) {
+        // all composites are distinct: output slot = number of selected composites above it
+        for (int i = tid; i < k; i += kTopkThreads) {
+            const uint64_t c = sel[i];
+            int rank = 0;
+            for (int q = 0; q < k; ++q) rank += sel[q] > c;
+            dst[rank] = (int32_t)(~(uint32_t)c);
         }
-        if (gt) {
-            const uint32_t p = atomicAdd(&s_gt, 1u);
-            sel[p] = ((uint64_t)o << 32) | (uint32_t)~(uint32_t)j;
-        }
-        const uint32_t r = block_rank(eq, warp_tot, &s_total);
-        if (eq && eq_base + r < need_eq)
-            sel[G + eq_base + r] = ((uint64_t)o << 32) | (uint32_t)~(uint32_t)j;
-        eq_base += s_total;
-        __syncthreads();
+        if (tid == 0 && counts) counts[row] = (int32_t)k;
+        return;
     }
     for (int i = (int)k + tid; i < sort_pow2; i += kTopkThreads) sel[i] = 0ull;
     __syncthreads();
@@ -161,7 +169,6 @@ k_topk_rows(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* __r
             __syncthreads();
         }
     }
-    int32_t* dst = idx_out + row * k;
     for (int i = tid; i < k; i += kTopkThreads) dst[i] = (int32_t)(~(uint32_t)sel[i]);
     if (tid == 0 && counts) counts[row] = (int32_t)k;
 }
