@@ -323,54 +323,31 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta,
         mbar_wait(done, 0);
         tc_fence_after();
         const uint32_t tacc = tmem + ((uint32_t)(quad * 32) << 16) + t * 128;
-        // Coalesced epilogue: each warp parks its 32 x 64 fp32 accumulator half-tile in the
-        // (now idle) stage buffers, then walks the rows with lanes along the columns, so the
-        // M_cache read-modify-write and the residual x_out = x_mid + M are 256-512 B
-        // contiguous per instruction instead of 32 scattered rows.
-        float* stg = reinterpret_cast<float*>(smem) + sw * (32 * 68);  // 32 rows x (64+4) f32
-        const int64_t row0 = (int64_t)b * p.n + (int64_t)c * p.chunk;
-        const int wrow0 = t * 128 + quad * 32;  // first chunk row of this warp
-        const int nrows = min(32, p.chunk - wrow0);
+        float* orow = p.out_cache + ((int64_t)b * p.n + (int64_t)c * p.chunk + r) * p.d + td * 128;
 #pragma unroll 1
-        for (int hf = 0; hf < 2; ++hf) {
+        for (int cc = 0; cc < 4; ++cc) {
             uint32_t acc[32];
+            tmem_ld32(tacc + cc * 32, acc);
+            tmem_ld_wait();
+            if (!row_ok) continue;
+            float4* o4 = reinterpret_cast<float4*>(orow + cc * 32);
+            float m[32];
+            float4 v[8];
 #pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-                tmem_ld32(tacc + hf * 64 + cc * 32, acc);
-                tmem_ld_wait();
-                float4* s4 = reinterpret_cast<float4*>(stg + lane * 68 + cc * 32);
+            for (int q = 0; q < 8; ++q) v[q] = o4[q];  // batch the loads
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    s4[q] = make_float4(__uint_as_float(acc[4 * q]), __uint_as_float(acc[4 * q + 1]),
-                                        __uint_as_float(acc[4 * q + 2]), __uint_as_float(acc[4 * q + 3]));
+            for (int q = 0; q < 8; ++q) {
+                v[q].x += __uint_as_float(acc[q * 4 + 0]);
+                v[q].y += __uint_as_float(acc[q * 4 + 1]);
+                v[q].z += __uint_as_float(acc[q * 4 + 2]);
+                v[q].w += __uint_as_float(acc[q * 4 + 3]);
+                m[q * 4 + 0] = v[q].x; m[q * 4 + 1] = v[q].y; m[q * 4 + 2] = v[q].z; m[q * 4 + 3] = v[q].w;
             }
-            __syncwarp();
-            // two rows per instruction: lanes 0-15 -> row rr, 16-31 -> row rr + 1, 4 cols each
-            const int sub = lane >> 4, c4 = (lane & 15) * 4;
-            for (int rr = 0; rr < nrows; rr += 2) {
-                const int lr = rr + sub;
-                if (lr < nrows) {
-                    const int64_t grow = row0 + wrow0 + lr;
-                    const int col = td * 128 + hf * 64 + c4;
-                    float4* o4 = reinterpret_cast<float4*>(p.out_cache + grow * p.d + col);
-                    const float4 a = *reinterpret_cast<const float4*>(stg + lr * 68 + c4);
-                    float4 v = *o4;
-                    v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
-                    *o4 = v;
-                    if (p.x_out != nullptr) {
-                        const uint2 xr = *reinterpret_cast<const uint2*>(p.x_mid + grow * p.d + col);
-                        const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xr);
-                        const float2 x0 = __bfloat1622float2(xh[0]), x1 = __bfloat1622float2(xh[1]);
-                        uint2 w;
-                        w.x = pack_bf16x2(x0.x + v.x, x0.y + v.y);
-                        w.y = pack_bf16x2(x1.x + v.z, x1.y + v.w);
-                        *reinterpret_cast<uint2*>(p.x_out + grow * p.d + col) = w;
-                    }
-                }
-            }
-            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o4[q] = v[q];
+            if (p.x_out != nullptr)
+                residual32(p, (int64_t)b * p.n + (int64_t)c * p.chunk + r, td * 128 + cc * 32, m);
         }
-        (void)row_ok;
     }
     tc_fence_before();
     __syncthreads();
