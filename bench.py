@@ -129,9 +129,17 @@ def run_ours(args, rank, world):
     bc = ops.BlockConfig(batch=cfg["batch"], seq=n, dim=cfg["dim"], heads=cfg["heads"],
                          head_dim=cfg["head_dim"], hidden=cfg["hidden"], chunk=cfg["chunk"],
                          attn_k=attn_k, mlp_k=mlp_k)
-    blk = ops.Block(bc, make_weights(cfg), production=True)
+    sharded = world > 1 or args.sharded
+    if sharded:
+        # heads + MLP hidden columns over the ranks; NCCL all-reduce of the Wo / W2 partials
+        # and all-gather of the MLP selection candidates (paper_2506_03275_b200/shard.py)
+        from paper_2506_03275_b200.shard import ShardedBlock, TorchComm
+        blk = ShardedBlock(bc, make_weights(cfg), TorchComm())
+    else:
+        blk = ops.Block(bc, make_weights(cfg), production=True)
     ctx = ops.context()
-    gen = torch.Generator(device="cuda").manual_seed(1235 + rank)
+    # the same latent on every rank (activations are replicated; the block is sharded)
+    gen = torch.Generator(device="cuda").manual_seed(1235)
     x = torch.randn((1, n, cfg["dim"]), device="cuda", generator=gen).to(torch.bfloat16)
     y = torch.empty_like(x)
     period = args.dense_interval + 1
@@ -233,17 +241,18 @@ def run_ours(args, rank, world):
             "warmup": args.warmup,
             "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": False,
-            "scaling": "weak" if world > 1 else "strong",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic (seeded N(0,1) latent, random-init weights per model.cpp:79-99)",
             "config": {
                 "workload": cfg["workload"], "model": "FLUX.1-dev-shaped block (1 layer)",
-                "global_batch": cfg["batch"] * world, "seq_len": n, "dim": cfg["dim"],
+                "global_batch": cfg["batch"], "seq_len": n, "dim": cfg["dim"],
                 "heads": cfg["heads"], "head_dim": cfg["head_dim"], "mlp_hidden": cfg["hidden"],
                 "chunk": cfg["chunk"], "voxel": list(cfg["voxel"]), "sparsity": cfg["sparsity"],
                 "attn_k": attn_k, "mlp_k": mlp_k, "dense_interval": args.dense_interval,
-                "parallelism": "replicas" if world > 1 else "single-gpu",
+                "parallelism": (f"heads/{world} + mlp-columns/{world}, NCCL all-reduce + "
+                                f"all-gather" if sharded else "single-gpu"),
                 "l2": "step inputs (x + 226 MB bf16 weights) exceed the 126 MB L2; attention "
                       "kernel reps flush L2 with a 256 MB write",
             },
@@ -444,6 +453,8 @@ def main():
     ap.add_argument("--dense-interval", type=int, default=10)
     ap.add_argument("--kernel-reps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the sharded block path even at one rank (runs under torchrun)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -453,11 +464,11 @@ def main():
         if res:
             print(json.dumps(res), flush=True)
         return
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
     res = run_ours(args, rank, world)
     if res is not None:
         if not args.no_cpu_baseline and world == 1:
@@ -469,7 +480,7 @@ def main():
                                    "kind": kind, "sample": desc,
                                    "sparse_step_ms": round(sp, 1), "dense_step_ms": round(de, 1)}
         print(json.dumps(res), flush=True)
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()

@@ -206,6 +206,29 @@ csd_status csd_block_destroy(csd_block* blk);
 csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int dense,
                           const int32_t* static_idx, const int32_t* static_counts,
                           int64_t static_k_max, void* stream);
+/* ---- Sharded execution (PROD): heads [head0, +heads_local) and neurons [f0, +f_local) per
+ * rank; the caller provides the collectives (NCCL over NVLink).  One step on rank r of g:
+ *   csd_block_attn_partial(x_in -> attn_partial)        ; all-reduce(sum) attn_partial
+ *   csd_residual_add(x_in, attn_partial -> x_mid)
+ *   dense : csd_block_mlp_dense_partial(x_mid -> mlp_partial)
+ *   sparse: csd_block_mlp_candidates(x_mid -> cand_scores, cand_ids [rows, k])
+ *           all-gather candidates in rank order -> [g, rows, k]
+ *           csd_block_mlp_sparse_partial(x_mid, all_scores, all_ids, g -> mlp_partial)
+ *   all-reduce(sum) mlp_partial ; csd_residual_add(x_mid, mlp_partial -> x_out)
+ * rows = B * N / chunk; k = cfg.mlp_k.  The merged selection is exactly the single-GPU
+ * per-chunk top-k (global id tie rule); each rank keeps its own neurons. */
+csd_status csd_block_attn_partial(csd_block* blk, const void* x_in, int dense,
+                                  float* attn_partial, void* stream);
+csd_status csd_block_mlp_dense_partial(csd_block* blk, const void* x_mid, float* mlp_partial,
+                                       void* stream);
+csd_status csd_block_mlp_candidates(csd_block* blk, const void* x_mid, float* cand_scores,
+                                    int32_t* cand_ids, void* stream);
+csd_status csd_block_mlp_sparse_partial(csd_block* blk, const void* x_mid,
+                                        const float* all_scores, const int32_t* all_ids,
+                                        int64_t world, float* mlp_partial, void* stream);
+/* out_bf16 = bf16(x_bf16 + partial_f32) (PROD residual after an all-reduce). */
+csd_status csd_residual_add(csd_ctx* ctx, const void* x, const float* partial, int64_t numel,
+                            void* out, void* stream);
 /* Cache views (reference layouts, fp32, device): which = 0 attn residual
  * [B,H,N,E], 1 row_max, 2 exp_sum [B,H,N], 3 mlp act [B,N,F], 4 mlp out
  * [B,N,D], 5 tile means [B,C,F]; 6/7 attention / mlp index sets (int32). */

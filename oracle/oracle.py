@@ -128,6 +128,15 @@ class Oracle:
                                              _L(voxel[0]), _L(voxel[1]), _L(voxel[2]), _f(out)))
         return out
 
+    # -- projections (port only; model.cpp:107-120) --------------------------
+    def project(self, x, w):
+        """x [B, N, D] @ w [D, Dout] with the reference's accumulation order."""
+        x, w = f32(x), f32(w)
+        b, n, d = x.shape
+        out = np.empty((b, n, w.shape[1]), np.float32)
+        self.lib.csdo_project(_f(x), _f(w), _L(b), _L(n), _L(d), _L(w.shape[1]), _f(out))
+        return out
+
     # -- selection ----------------------------------------------------------
     def select_top_k(self, scores, k):
         s = f32(scores)

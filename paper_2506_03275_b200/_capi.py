@@ -68,6 +68,11 @@ SIGNATURES = {
     "csd_block_destroy": (i32, [p]),
     "csd_block_step": (i32, [p, fp, fp, C.c_int, fp, fp, i64, p]),
     "csd_block_cache": (i32, [p, C.c_int, fp, fp, p]),
+    "csd_block_attn_partial": (i32, [p, fp, C.c_int, fp, p]),
+    "csd_block_mlp_dense_partial": (i32, [p, fp, fp, p]),
+    "csd_block_mlp_candidates": (i32, [p, fp, fp, fp, p]),
+    "csd_block_mlp_sparse_partial": (i32, [p, fp, fp, fp, i64, fp, p]),
+    "csd_residual_add": (i32, [p, fp, fp, i64, fp, p]),
 }
 
 

@@ -98,6 +98,10 @@ csd_status upload(csd_block* blk, void** dst, const float* host, int64_t rows, i
 
 }  // namespace
 
+static csd_status attn_core(csd_block* blk, const void* x_in, int dense, const int32_t* static_idx,
+                            const int32_t* static_counts, int64_t static_k_max, void* stream);
+static csd_status sparse_mlp_apply(csd_block* blk, const void* x_mid, void* x_out, cudaStream_t s);
+
 extern "C" {
 
 csd_status csd_block_create(csd_ctx* ctx, csd_mode mode, const csd_block_config* cfg_in,
@@ -191,11 +195,66 @@ csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int den
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (!dense && (!blk->attn_init || !blk->mlp_init))
         return set_error(CSD_ERR_STATE, "sparse attention step requested before any dense step");
-    const int64_t B = c.batch, N = c.seq, D = c.dim, E = c.head_dim, Hl = c.heads_local;
-    const int64_t Dl = Hl * E, Fl = c.f_local, C = N / c.chunk;
-    const int64_t ak = blk->a_kmax;
+    const int64_t B = c.batch, N = c.seq, D = c.dim;
+    const int64_t Dl = c.heads_local * c.head_dim, Fl = c.f_local;
     const int64_t mk = c.mlp_k > 0 ? c.mlp_k : Fl;
-    // ---- attention branch
+    CSD_TRY(attn_core(blk, x_in, dense, static_idx, static_counts, static_k_max, stream));
+    if (md == CSD_MODE_PROD) {
+        // x1 = x + O Wo: the residual rides in the GEMM (C = x, beta = 1, fp32 accumulate)
+        CSD_CU(cudaMemcpyAsync(blk->x_mid, x_in, 2 * B * N * D, cudaMemcpyDeviceToDevice, s), "copy");
+        CSD_TRY(csd::gemm_bf16(blk->ctx, blk->attn, blk->wo, false, blk->x_mid, false, B * N, D, Dl,
+                               1.0f, s));
+        // ---- MLP branch; x2 = x1 + M is fused into the last MLP kernel's epilogue
+        if (dense) {
+            CSD_TRY(csd::prod_dense_mlp(blk->ctx, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B,
+                                        N, D, Fl, c.chunk, blk->mout, blk->act, blk->x_mid, x_out,
+                                        s));
+            CSD_TRY(csd_mlp_tile_means(ctx, md, blk->x_mid, blk->w1, B, N, D, Fl, c.chunk,
+                                       blk->tmeans, stream));
+            blk->mlp_init = true;
+            blk->mlp_age = 0;
+        } else {
+            CSD_TRY(csd_mlp_change_indices(ctx, md, blk->x_mid, blk->w1, blk->tmeans, B, N, D, Fl,
+                                           mk, c.chunk, blk->midx, blk->mcnt, stream));
+            CSD_TRY(sparse_mlp_apply(blk, blk->x_mid, x_out, s));
+        }
+        return CSD_OK;
+    }
+    // ---------------- CHECK mode: op for op as model.cpp:200-213
+    CSD_TRY(csd_project(ctx, md, blk->attn, blk->wo, B, N, Dl, D, blk->proj, stream));
+    CSD_TRY(csd_add(ctx, md, x_in, blk->proj, B * N * D, blk->x_mid, stream));
+    if (dense) {
+        CSD_TRY(csd_dense_mlp(ctx, md, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B, N, D, Fl,
+                              c.chunk, blk->mout, blk->act, stream));
+        CSD_TRY(csd_mlp_tile_means(ctx, md, blk->x_mid, blk->w1, B, N, D, Fl, c.chunk, blk->tmeans,
+                                   stream));
+        blk->mlp_init = true;
+        blk->mlp_age = 0;
+    } else {
+        CSD_TRY(csd_mlp_change_indices(ctx, md, blk->x_mid, blk->w1, blk->tmeans, B, N, D, Fl, mk,
+                                       c.chunk, blk->midx, blk->mcnt, stream));
+        CSD_TRY(csd_sparse_delta_mlp(ctx, md, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->midx,
+                                     blk->mcnt, mk, c.chunk, B, N, D, Fl, blk->act, blk->mout,
+                                     stream));
+        blk->mlp_age += 1;
+    }
+    CSD_TRY(csd_add(ctx, md, blk->x_mid, blk->mout, B * N * D, x_out, stream));
+    return CSD_OK;
+}
+
+}  // extern "C"
+
+// ---- attention branch of a step (shared by the whole-block and the sharded paths):
+// q,k,v for the block's heads, then colsum/top-k/cache-init (dense) or the sparse delta.
+static csd_status attn_core(csd_block* blk, const void* x_in, int dense, const int32_t* static_idx,
+                            const int32_t* static_counts, int64_t static_k_max, void* stream) {
+    const auto& c = blk->cfg;
+    csd_ctx* ctx = reinterpret_cast<csd_ctx*>(blk->ctx);
+    const csd_mode md = blk->mode;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t B = c.batch, N = c.seq, D = c.dim, E = c.head_dim, Hl = c.heads_local;
+    const int64_t Dl = Hl * E, C = N / c.chunk;
+    const int64_t ak = blk->a_kmax;
     CSD_TRY(csd_project(ctx, md, x_in, blk->wq, B, N, D, Dl, blk->q, stream));
     CSD_TRY(csd_project(ctx, md, x_in, blk->wk, B, N, D, Dl, blk->k, stream));
     CSD_TRY(csd_project(ctx, md, x_in, blk->wv, B, N, D, Dl, blk->v, stream));
@@ -252,56 +311,116 @@ csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int den
                                            Hl, N, E, blk->attn, stream));
         blk->attn_age += 1;
     }
-    if (md == CSD_MODE_PROD) {
-        // x1 = x + O Wo: the residual rides in the GEMM (C = x, beta = 1, fp32 accumulate)
-        CSD_CU(cudaMemcpyAsync(blk->x_mid, x_in, 2 * B * N * D, cudaMemcpyDeviceToDevice, s), "copy");
-        CSD_TRY(csd::gemm_bf16(blk->ctx, blk->attn, blk->wo, false, blk->x_mid, false, B * N, D, Dl,
-                               1.0f, s));
-        // ---- MLP branch; x2 = x1 + M is fused into the last MLP kernel's epilogue
-        if (dense) {
-            CSD_TRY(csd::prod_dense_mlp(blk->ctx, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B,
-                                        N, D, Fl, c.chunk, blk->mout, blk->act, blk->x_mid, x_out,
-                                        s));
-            CSD_TRY(csd_mlp_tile_means(ctx, md, blk->x_mid, blk->w1, B, N, D, Fl, c.chunk,
-                                       blk->tmeans, stream));
-            blk->mlp_init = true;
-            blk->mlp_age = 0;
-        } else {
-            CSD_TRY(csd_mlp_change_indices(ctx, md, blk->x_mid, blk->w1, blk->tmeans, B, N, D, Fl,
-                                           mk, c.chunk, blk->midx, blk->mcnt, stream));
-            if (!mlp_tc_supported(D, c.chunk))
-                return set_error(CSD_ERR_UNSUPPORTED, "sparse-delta MLP envelope (D %% 128, chunk <= 256)");
-            const int64_t k_pad = (mk + 127) / 128 * 128;
-            void* dws = blk->ctx->ws(csd::kWsDelta, 2 * B * N * k_pad);
-            if (!dws) return set_error(CSD_ERR_CUDA, "workspace allocation failed");
-            CSD_CU(prod_sparse_delta_mlp_tc(blk->x_mid, blk->w1, blk->b1, blk->w2, blk->midx,
-                                            blk->mcnt, mk, c.chunk, B, N, D, Fl, blk->act,
-                                            blk->mout, dws, s, blk->x_mid, x_out),
-                   "sparse_delta_mlp");
-            blk->ctx->launches += 2;
-            blk->mlp_age += 1;
-        }
-        return CSD_OK;
-    }
-    // ---------------- CHECK mode: op for op as model.cpp:200-213
-    CSD_TRY(csd_project(ctx, md, blk->attn, blk->wo, B, N, Dl, D, blk->proj, stream));
-    CSD_TRY(csd_add(ctx, md, x_in, blk->proj, B * N * D, blk->x_mid, stream));
-    if (dense) {
-        CSD_TRY(csd_dense_mlp(ctx, md, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B, N, D, Fl,
-                              c.chunk, blk->mout, blk->act, stream));
-        CSD_TRY(csd_mlp_tile_means(ctx, md, blk->x_mid, blk->w1, B, N, D, Fl, c.chunk, blk->tmeans,
-                                   stream));
-        blk->mlp_init = true;
-        blk->mlp_age = 0;
-    } else {
-        CSD_TRY(csd_mlp_change_indices(ctx, md, blk->x_mid, blk->w1, blk->tmeans, B, N, D, Fl, mk,
-                                       c.chunk, blk->midx, blk->mcnt, stream));
-        CSD_TRY(csd_sparse_delta_mlp(ctx, md, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->midx,
-                                     blk->mcnt, mk, c.chunk, B, N, D, Fl, blk->act, blk->mout,
-                                     stream));
-        blk->mlp_age += 1;
-    }
-    CSD_TRY(csd_add(ctx, md, blk->x_mid, blk->mout, B * N * D, x_out, stream));
+    return CSD_OK;
+}
+
+// ---- PROD sparse-delta MLP with the block's current index set (midx / mcnt); optional
+// fused residual x_out = x_mid + M_cache.
+static csd_status sparse_mlp_apply(csd_block* blk, const void* x_mid, void* x_out, cudaStream_t s) {
+    const auto& c = blk->cfg;
+    const int64_t B = c.batch, N = c.seq, D = c.dim, Fl = c.f_local;
+    const int64_t mk = c.mlp_k > 0 ? c.mlp_k : Fl;
+    if (!mlp_tc_supported(D, c.chunk))
+        return set_error(CSD_ERR_UNSUPPORTED, "sparse-delta MLP envelope (D %% 128, chunk <= 256)");
+    const int64_t k_pad = (mk + 127) / 128 * 128;
+    void* dws = blk->ctx->ws(csd::kWsDelta, 2 * B * N * k_pad);
+    if (!dws) return set_error(CSD_ERR_CUDA, "workspace allocation failed");
+    CSD_CU(prod_sparse_delta_mlp_tc(x_mid, blk->w1, blk->b1, blk->w2, blk->midx, blk->mcnt, mk,
+                                    c.chunk, B, N, D, Fl, blk->act, blk->mout, dws, s, x_mid, x_out),
+           "sparse_delta_mlp");
+    blk->ctx->launches += 2;
+    blk->mlp_age += 1;
+    return CSD_OK;
+}
+
+extern "C" {
+
+// ---------------------------------------------------------------- sharded execution
+csd_status csd_block_attn_partial(csd_block* blk, const void* x_in, int dense,
+                                  float* attn_partial, void* stream) {
+    if (!blk) return set_error(CSD_ERR_VALUE, "null block");
+    if (blk->mode != CSD_MODE_PROD) return set_error(CSD_ERR_UNSUPPORTED, "sharded steps are PROD only");
+    if (!dense && !blk->attn_init)
+        return set_error(CSD_ERR_STATE, "sparse attention step requested before any dense step");
+    const auto& c = blk->cfg;
+    CSD_TRY(attn_core(blk, x_in, dense, nullptr, nullptr, 0, stream));
+    // this rank's heads through its rows of Wo: a partial [B, N, D] sum (all-reduced by the caller)
+    return csd::gemm_bf16(blk->ctx, blk->attn, blk->wo, false, attn_partial, true, c.batch * c.seq,
+                          c.dim, c.heads_local * c.head_dim, 0.0f, static_cast<cudaStream_t>(stream));
+}
+
+csd_status csd_block_mlp_dense_partial(csd_block* blk, const void* x_mid, float* mlp_partial,
+                                       void* stream) {
+    if (!blk) return set_error(CSD_ERR_VALUE, "null block");
+    if (blk->mode != CSD_MODE_PROD) return set_error(CSD_ERR_UNSUPPORTED, "sharded steps are PROD only");
+    const auto& c = blk->cfg;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t B = c.batch, N = c.seq, D = c.dim, Fl = c.f_local;
+    CSD_TRY(csd::prod_dense_mlp(blk->ctx, x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B, N, D, Fl,
+                                c.chunk, blk->mout, blk->act, nullptr, nullptr, s));
+    CSD_TRY(csd_mlp_tile_means(reinterpret_cast<csd_ctx*>(blk->ctx), blk->mode, x_mid, blk->w1, B, N,
+                               D, Fl, c.chunk, blk->tmeans, stream));
+    CSD_CU(cudaMemcpyAsync(mlp_partial, blk->mout, 4 * B * N * D, cudaMemcpyDeviceToDevice, s), "copy");
+    blk->mlp_init = true;
+    blk->mlp_age = 0;
+    return CSD_OK;
+}
+
+csd_status csd_block_mlp_candidates(csd_block* blk, const void* x_mid, float* cand_scores,
+                                    int32_t* cand_ids, void* stream) {
+    if (!blk) return set_error(CSD_ERR_VALUE, "null block");
+    if (blk->mode != CSD_MODE_PROD) return set_error(CSD_ERR_UNSUPPORTED, "sharded steps are PROD only");
+    if (!blk->mlp_init) return set_error(CSD_ERR_STATE, "sparse MLP step requested before any dense step");
+    const auto& c = blk->cfg;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t B = c.batch, N = c.seq, D = c.dim, Fl = c.f_local, rows = B * (N / c.chunk);
+    const int64_t k = c.mlp_k > 0 ? c.mlp_k : c.hidden;
+    const int64_t k_loc = k < Fl ? k : Fl;
+    float* scores = (float*)blk->ctx->ws(csd::kWsScores, 4 * rows * Fl);
+    void* ws = blk->ctx->ws(csd::kWsMeans, prod_means_ws_bytes(B, N, D, Fl, c.chunk));
+    int32_t* ids = (int32_t*)blk->ctx->ws(csd::kWsIdx, 4 * rows * k_loc);
+    int32_t* cnt = (int32_t*)blk->ctx->ws(csd::kWsCounts, 4 * rows);
+    if (!scores || !ws || !ids || !cnt) return set_error(CSD_ERR_CUDA, "workspace allocation failed");
+    // local |T - T_m| (mlp.cpp:116) and the shard's top-k
+    CSD_CU(prod_tile_means_tc(x_mid, blk->w1, B, N, D, Fl, c.chunk, blk->tmeans, scores, ws, s),
+           "tile_means");
+    CSD_CU(topk_rows(scores, rows, Fl, k_loc, ids, cnt, s), "topk");
+    CSD_CU(shard_candidates(ids, scores, rows, Fl, k_loc, k, c.f0, cand_scores, cand_ids, s),
+           "candidates");
+    blk->ctx->launches += 5;
+    return CSD_OK;
+}
+
+csd_status csd_block_mlp_sparse_partial(csd_block* blk, const void* x_mid,
+                                        const float* all_scores, const int32_t* all_ids,
+                                        int64_t world, float* mlp_partial, void* stream) {
+    if (!blk) return set_error(CSD_ERR_VALUE, "null block");
+    if (blk->mode != CSD_MODE_PROD) return set_error(CSD_ERR_UNSUPPORTED, "sharded steps are PROD only");
+    if (!blk->mlp_init) return set_error(CSD_ERR_STATE, "sparse MLP step requested before any dense step");
+    if (world < 1) return set_error(CSD_ERR_VALUE, "world size must be >= 1");
+    const auto& c = blk->cfg;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t B = c.batch, N = c.seq, D = c.dim, rows = B * (N / c.chunk);
+    const int64_t k = c.mlp_k > 0 ? c.mlp_k : c.hidden;
+    float* ws_s = (float*)blk->ctx->ws(csd::kWsLogits, 4 * rows * world * k);
+    int32_t* ws_i = (int32_t*)blk->ctx->ws(csd::kWsProbs, 4 * rows * world * k);
+    int32_t* ws_p = (int32_t*)blk->ctx->ws(csd::kWsIdx, 4 * rows * k);
+    int32_t* ws_c = (int32_t*)blk->ctx->ws(csd::kWsCounts, 4 * rows);
+    if (!ws_s || !ws_i || !ws_p || !ws_c) return set_error(CSD_ERR_CUDA, "workspace allocation failed");
+    const int64_t mk = c.mlp_k > 0 ? c.mlp_k : c.f_local;  // row stride of midx
+    CSD_CU(shard_merge(all_scores, all_ids, world, rows, k, c.f0, c.f_local, ws_s, ws_i, ws_p, ws_c,
+                       blk->midx, mk, blk->mcnt, s),
+           "merge");
+    blk->ctx->launches += 3;
+    CSD_TRY(sparse_mlp_apply(blk, x_mid, nullptr, s));
+    CSD_CU(cudaMemcpyAsync(mlp_partial, blk->mout, 4 * B * N * D, cudaMemcpyDeviceToDevice, s), "copy");
+    return CSD_OK;
+}
+
+csd_status csd_residual_add(csd_ctx* ctx, const void* x, const float* partial, int64_t numel,
+                            void* out, void* stream) {
+    CSD_CU(prod_add_bf16_f32(x, partial, numel, out, static_cast<cudaStream_t>(stream)), "add");
+    reinterpret_cast<Ctx*>(ctx)->launches += 1;
     return CSD_OK;
 }
 

@@ -58,6 +58,14 @@ cudaError_t topk_rows_global(const float* scores, int64_t rows, int64_t m, int64
                              int32_t* idx, int32_t* counts, uint64_t* ws, cudaStream_t s);
 cudaError_t validate_index_set(const int32_t* idx, const int32_t* counts, int64_t rows,
                                int64_t k_max, int64_t domain, uint32_t* flags, cudaStream_t s);
+// shard.cu (F-sharded exact selection)
+cudaError_t shard_candidates(const int32_t* ids, const float* scores, int64_t rows, int64_t m,
+                             int64_t k_loc, int64_t k_out, int64_t id_offset, float* cand_scores,
+                             int32_t* cand_ids, cudaStream_t s);
+cudaError_t shard_merge(const float* all_scores, const int32_t* all_ids, int64_t g, int64_t rows,
+                        int64_t k, int64_t f0, int64_t f_local, float* ws_scores, int32_t* ws_ids,
+                        int32_t* ws_pos, int32_t* ws_cnt, int32_t* idx, int64_t ld_idx,
+                        int32_t* counts, cudaStream_t s);
 // voxel.cu
 cudaError_t voxel_reorder(const void* src, void* dst, int64_t batch, int64_t t, int64_t h,
                           int64_t w, int64_t vt, int64_t vh, int64_t vw, int64_t row_bytes,

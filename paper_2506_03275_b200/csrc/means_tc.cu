@@ -147,15 +147,10 @@ __global__ void k_means_reduce(const float* __restrict__ partial, int ksplit, in
     out[i] = cached ? fabsf(s - cached[i]) : s;
 }
 
-static int pick_ksplit(int64_t tiles, int64_t kblocks) {
-    int best = 1;
-    for (int k = 1; k <= 8; ++k) {
-        if (kblocks % k) continue;
-        best = k;
-        if (tiles * k >= 148) break;
-    }
-    return best;
-}
+// The split depends on D only — never on the neuron count — so a hidden-column shard
+// (F/g neurons on each of g GPUs) produces bit-identical T values and therefore the same
+// global top-k as one GPU.
+static int pick_ksplit(int64_t /*tiles*/, int64_t kblocks) { return kblocks % 2 == 0 ? 2 : 1; }
 
 // T (or |T - cached| when cached != null) for the chunk means of x.
 // ws: bop [ntiles*128, D] bf16 + partials [ksplit][BC][F] fp32 (see prod_means_ws_bytes).
