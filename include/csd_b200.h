@@ -182,7 +182,7 @@ csd_status csd_add(csd_ctx* ctx, csd_mode mode, const void* a, const void* b, in
  * (AttentionCache / MlpCache, attention.hpp:13-19, mlp.hpp:29-36).
  * Head / hidden sharding: a block may own heads [head0, head0+heads_local)
  * and neurons [f0, f0+f_local) (csd_block_config); sharded execution is
- * driven through csd_block_step_partial (see below). */
+ * driven through the csd_block_*_partial calls below. */
 typedef struct {
     int64_t batch, seq, dim, heads, head_dim, hidden, chunk;
     int64_t attn_k, mlp_k;   /* per-chunk keys / neurons recomputed */

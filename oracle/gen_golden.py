@@ -143,6 +143,20 @@ def main():
             mi, mc = M.indices(0, True, mlp_k)
             bl[f"midx{t}"] = mi
     np.savez_compressed(os.path.join(OUT, "block.npz"), **bl)
+
+    # ---- block stack through model_forward_step (model.hpp defaults, 2 layers), fed back
+    # step to step like harness.cpp:186-212; tests/cpp/model_mirror.cpp replays it
+    cfg = dict(batch=1, grid=(2, 8, 8), dim=64, head_dim=16, heads=4, hidden=128, layers=2,
+               voxel=(1, 2, 2), chunk=4, seed=1234)
+    M = O.RefModel(cfg)
+    x = g(1235, (1, M.n, cfg["dim"]))
+    ms = {"x": x}
+    cur = x
+    for t, dense in enumerate([1, 0, 0, 1, 0]):
+        cur = M.step(cur, dense, 8, 32)
+        ms[f"y{t}"] = cur
+    ms["dense"] = M.dense(x)
+    np.savez_compressed(os.path.join(OUT, "model_stack.npz"), **ms)
     for fn in sorted(os.listdir(OUT)):
         print(fn, os.path.getsize(os.path.join(OUT, fn)))
 

@@ -19,6 +19,8 @@
 #include "csd/attention.hpp"
 #include "csd/metrics.hpp"
 #include "csd/mlp.hpp"
+#include "csd/model.hpp"
+#include "csd/rng.hpp"
 #include "csd/voxel.hpp"
 #include "csd_b200.h"
 
@@ -553,6 +555,154 @@ Tensor mlp_step(const Tensor& x, const MlpWeights& w, MlpCache& cache, bool dens
     Tensor out = sparse_delta_mlp(x, w, idx, cache);
     cache.indices = std::move(idx);
     return out;
+}
+
+
+// ====================================================================== block stack
+// model.cpp:10-216.  Projections run on the device (csd_project, CHECK mode: the
+// reference's sequential-k fp32 gemm); attention_step / mlp_step are the device-backed
+// routines above; head split/merge and the residual add are host data movement / fp32 adds.
+void ModelConfig::validate() const {  // model.cpp:10-28
+    if (batch < 1 || grid_t < 1 || grid_h < 1 || grid_w < 1 || model_dim < 1 || head_dim < 1 ||
+        heads < 1 || mlp_hidden < 1 || layers < 0 || chunk < 1)
+        throw ConfigError("model config fields must be positive (layers may be 0)");
+    if (model_dim != heads * head_dim)
+        throw ConfigError("model_dim " + std::to_string(model_dim) + " != heads*head_dim " +
+                          std::to_string(heads * head_dim));
+    if (seq_len() % chunk != 0)
+        throw ConfigError("sequence length " + std::to_string(seq_len()) +
+                          " not divisible by chunk " + std::to_string(chunk));
+    if (voxel_t * voxel_h * voxel_w != chunk)
+        throw ConfigError("voxel volume " + std::to_string(voxel_t * voxel_h * voxel_w) +
+                          " must equal chunk " + std::to_string(chunk));
+    voxel_layout().validate();
+}
+
+namespace {
+Tensor draw(GaussianRng& rng, std::vector<int64_t> shape, float stddev) {
+    Tensor t(std::move(shape));
+    for (int64_t i = 0; i < t.numel(); ++i) t[i] = rng.next(0.0f, stddev);
+    return t;
+}
+Tensor residual_add(const Tensor& a, const Tensor& b) {  // model.cpp:47-57
+    if (a.shape() != b.shape())
+        throw ShapeError("residual add shapes disagree: " + shape_str(a.shape()) + " vs " +
+                         shape_str(b.shape()));
+    Tensor out = a;
+    for (int64_t i = 0; i < out.numel(); ++i) out[i] += b[i];
+    return out;
+}
+struct Qkv {
+    Tensor q, k, v;
+};
+Qkv project_qkv(const LayerWeights& lw, const Tensor& x, int64_t heads, int64_t head_dim) {
+    return {split_heads(project(x, lw.wq), heads, head_dim),
+            split_heads(project(x, lw.wk), heads, head_dim),
+            split_heads(project(x, lw.wv), heads, head_dim)};
+}
+}  // namespace
+
+ToyModel build_toy_model(const ModelConfig& cfg) {  // model.cpp:79-99 (draw order, 0.5 gain)
+    cfg.validate();
+    ToyModel m;
+    m.cfg = cfg;
+    GaussianRng rng(cfg.seed);
+    const float s = 1.0f / std::sqrt(static_cast<float>(cfg.model_dim)), so = 0.5f * s;
+    const int64_t d = cfg.model_dim, f = cfg.mlp_hidden;
+    for (int64_t l = 0; l < cfg.layers; ++l) {
+        LayerWeights lw;
+        lw.wq = draw(rng, {d, d}, s);
+        lw.wk = draw(rng, {d, d}, s);
+        lw.wv = draw(rng, {d, d}, s);
+        lw.wo = draw(rng, {d, d}, so);
+        lw.mlp.w1 = draw(rng, {f, d}, s);
+        lw.mlp.b1 = draw(rng, {f}, s);
+        lw.mlp.w2 = draw(rng, {f, d}, so);
+        lw.mlp.b2 = draw(rng, {d}, so);
+        m.layers.push_back(std::move(lw));
+    }
+    return m;
+}
+
+ModelState make_state(const ToyModel& model) {
+    ModelState st;
+    st.layers.resize(model.layers.size());
+    return st;
+}
+
+Tensor project(const Tensor& x, const Tensor& w) {  // model.cpp:107-120
+    if (x.rank() != 3) throw ShapeError("project expects [B x N x D] input, got " + shape_str(x.shape()));
+    if (w.rank() != 2 || w.dim(0) != x.dim(2))
+        throw ShapeError("gemm inner dimensions disagree: " + shape_str({x.dim(1), x.dim(2)}) +
+                         " @ " + shape_str(w.shape()));
+    const int64_t b = x.dim(0), n = x.dim(1), d = x.dim(2), dout = w.dim(1);
+    Tensor out({b, n, dout});
+    Dev dx(x), dw(w), dout_(sizeof(float) * out.numel());
+    ok(csd_project(ctx(), CSD_MODE_CHECK, dx.v(), dw.v(), b, n, d, dout, dout_.v(), nullptr));
+    dout_.to(out);
+    return out;
+}
+
+Tensor split_heads(const Tensor& x, int64_t heads, int64_t head_dim) {  // model.cpp:122-143
+    if (x.rank() != 3 || x.dim(2) != heads * head_dim)
+        throw ShapeError("split_heads: input " + shape_str(x.shape()) + " does not factor into " +
+                         std::to_string(heads) + " heads of dim " + std::to_string(head_dim));
+    const int64_t b = x.dim(0), n = x.dim(1);
+    Tensor out({b, heads, n, head_dim});
+    for (int64_t bb = 0; bb < b; ++bb)
+        for (int64_t h = 0; h < heads; ++h)
+            for (int64_t t = 0; t < n; ++t)
+                std::memcpy(out.data() + ((bb * heads + h) * n + t) * head_dim,
+                            x.data() + ((bb * n + t) * heads + h) * head_dim, sizeof(float) * head_dim);
+    return out;
+}
+
+Tensor merge_heads(const Tensor& x) {  // model.cpp:145-165
+    if (x.rank() != 4) throw ShapeError("merge_heads expects [B x H x N x E], got " + shape_str(x.shape()));
+    const int64_t b = x.dim(0), heads = x.dim(1), n = x.dim(2), e = x.dim(3);
+    Tensor out({b, n, heads * e});
+    for (int64_t bb = 0; bb < b; ++bb)
+        for (int64_t h = 0; h < heads; ++h)
+            for (int64_t t = 0; t < n; ++t)
+                std::memcpy(out.data() + ((bb * n + t) * heads + h) * e,
+                            x.data() + ((bb * heads + h) * n + t) * e, sizeof(float) * e);
+    return out;
+}
+
+Tensor model_forward_dense(const ToyModel& model, const Tensor& x) {  // model.cpp:167-176
+    Tensor cur = x;
+    for (const auto& lw : model.layers) {
+        const Qkv p = project_qkv(lw, cur, model.cfg.heads, model.cfg.head_dim);
+        cur = residual_add(cur, project(merge_heads(dense_attention(p.q, p.k, p.v)), lw.wo));
+        cur = residual_add(cur, dense_mlp(cur, lw.mlp).output);
+    }
+    return cur;
+}
+
+Tensor model_forward_step(const ToyModel& model, ModelState& state, const Tensor& x,
+                          bool dense_step, const SparsityConfig& sparsity, LayerProbe* probe,
+                          const SparseIndexSet* static_attn) {  // model.cpp:178-216
+    if (state.layers.size() != model.layers.size())
+        throw StateError("model state layer count does not match the model");
+    Tensor cur = x;
+    for (size_t l = 0; l < model.layers.size(); ++l) {
+        const auto& lw = model.layers[l];
+        LayerState& ls = state.layers[l];
+        const Qkv p = project_qkv(lw, cur, model.cfg.heads, model.cfg.head_dim);
+        const Tensor a = attention_step(p.q, p.k, p.v, ls.attn, dense_step, sparsity.attn_k,
+                                        model.cfg.chunk, static_attn);
+        if (probe)
+            probe->attention_sample(static_cast<int64_t>(l), dense_step,
+                                    dense_step ? a : dense_attention(p.q, p.k, p.v), a);
+        cur = residual_add(cur, project(merge_heads(a), lw.wo));
+        const Tensor mlp_in = cur;
+        const Tensor m = mlp_step(mlp_in, lw.mlp, ls.mlp, dense_step, sparsity.mlp_k, model.cfg.chunk);
+        if (probe)
+            probe->mlp_sample(static_cast<int64_t>(l), dense_step,
+                              dense_step ? m : dense_mlp(mlp_in, lw.mlp).output, m);
+        cur = residual_add(cur, m);
+    }
+    return cur;
 }
 
 }  // namespace csd

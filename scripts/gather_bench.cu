@@ -18,7 +18,10 @@
 
 using namespace csd::tc;
 
-constexpr int kStages = 4;
+#ifndef STAGES
+#define STAGES 4
+#endif
+constexpr int kStages = STAGES;
 constexpr int kBlk = 128 * 128;
 
 __global__ void __launch_bounds__(512, 1)
@@ -32,7 +35,7 @@ k_bench(const __grid_constant__ CUtensorMap tile_map, const __grid_constant__ CU
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(full + s, mode == 5 ? 128 : 1);
+            mbar_init(full + s, mode == 5 ? 128 : mode == 6 ? 65 : 1);
             mbar_init(empty + s, blockDim.x / 32);
         }
         fence_barrier_init();
@@ -76,6 +79,24 @@ k_bench(const __grid_constant__ CUtensorMap tile_map, const __grid_constant__ CU
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 128, [%2];"
                 ::"r"(smem_u32(dst + row * 128)), "l"(src), "r"(smem_u32(full + s)) : "memory");
+            }
+        } else if (mode == 6) {
+            // mixed: rows [0,64) by TMA gather4 (warps 0-3, 4 instructions each), rows
+            // [64,128) by cp.async 16 B (threads 128..191, one row x 8 chunks each)
+            if (threadIdx.x == 0) mbar_arrive_expect_tx(full + s, kBlk / 2);
+            __syncthreads();
+            if (warp < 4 && lane < 4) {
+                const int g = warp * 4 + lane;
+                const int* r = rows + rbase + g * 4;
+                tma_gather4(&g4_map, full + s, dst + g * 512, 0, r[0], r[1], r[2], r[3]);
+            } else if (threadIdx.x >= 128 && threadIdx.x < 192) {
+                const int row = 64 + threadIdx.x - 128;
+                const uint8_t* src = reinterpret_cast<const uint8_t*>(base + (size_t)rows[rbase + row] * ld);
+                for (int c = 0; c < 8; ++c) {
+                    const uint32_t d = smem_u32(dst) + sw128_offset(row, c);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c * 16));
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)));
             }
         } else {  // mode 5
             // 128 threads x 8 x 16 B; row = tid, chunks 0..7 swizzled
@@ -148,6 +169,10 @@ int main(int argc, char** argv) {
         {"tma gather4 16 warps x2 (random, L2)", 3, rows_l2, 512},
         {"tma gather4 8 warps x4 (random, DRAM)", 3, rows, 256},
         {"tma gather4 16 warps x2 (random, DRAM)", 3, rows, 512},
+        {"cp.async 128 thr (random, L2)", 5, rows_l2, 128},
+        {"cp.async 128 thr (random, DRAM)", 5, rows, 128},
+        {"mixed g4 4 warps + cp.async 64 thr (L2)", 6, rows_l2, 256},
+        {"mixed g4 4 warps + cp.async 64 thr (DRAM)", 6, rows, 256},
     };
     for (const Case& cs : cases) {
         const int mode = cs.mode;

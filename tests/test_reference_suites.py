@@ -1,9 +1,12 @@
-"""The reference's OWN unit-test programs, compiled unmodified against our C++ csd:: mirror.
+"""The reference's OWN test programs, compiled unmodified against our C++ csd:: mirror.
 
 `make -C oracle reftests` (run by __graft_entry__.build() when /root/reference is present)
-compiles /root/reference/proj/tests/test_{voxel,attention,mlp}.cpp with include/csd/*.hpp
-and links them to paper_2506_03275_b200/libcsd_host.so, whose voxel / top-k / attention /
-MLP calls execute the CUDA kernels of libcsd_b200.so (CHECK mode).  Each program aborts on
+compiles all eight /root/reference/proj/tests programs (the unit suites and acceptance.cpp)
+with include/csd/*.hpp first on the include path and links them to
+paper_2506_03275_b200/libcsd_host.so, whose tensor / voxel / top-k / attention / MLP / block
+calls execute the CUDA kernels of libcsd_b200.so (CHECK mode); the reference's own
+non-hot-path units (harness, schedule, bitmask, memory, ...) are compiled alongside, as a
+maintainer switching the reference build over would.  Each program aborts on
 the first failed CHECK, so exit code 0 + its "tests passed" line is the whole verdict: the
 drop-in library satisfies the reference's own test suite (incl. its 64-bit oracles, tie
 rules, error types and bit-exact identities).
@@ -18,14 +21,20 @@ BIN = os.path.join(ROOT, "oracle", "_ref", "reftests")
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite,banner", [("test_voxel", "voxel tests passed"),
-                                          ("test_attention", "attention tests passed"),
-                                          ("test_mlp", "mlp tests passed")])
+@pytest.mark.parametrize("suite,banner", [
+    ("test_tensor", "tensor tests passed"),
+    ("test_voxel", "voxel tests passed"),
+    ("test_attention", "attention tests passed"),
+    ("test_mlp", "mlp tests passed"),
+    ("test_cache_store", "cache-store tests passed"),
+    ("test_schedule", "schedule/flops/metrics tests passed"),
+    ("test_harness", "harness tests passed"),
+    ("acceptance", "all acceptance criteria passed")])
 def test_reference_suite_on_b200(suite, banner):
     exe = os.path.join(BIN, suite)
     if not os.path.exists(exe):
         pytest.skip("reference test programs not built (needs /root/reference at build time)")
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900, cwd=BIN)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert banner in r.stdout
 
