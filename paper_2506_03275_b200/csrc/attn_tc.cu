@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <mutex>
 
@@ -36,6 +37,17 @@ namespace csd {
 namespace dev {
 
 using namespace csd::tc;
+
+// Debug timeline (scripts/attn_trace.py): when set, CTAs < kTraceCtas record SM clock64()
+// stamps at fixed slots (start, Q / K / V issue, S issue, softmax and epilogue phases).
+constexpr int kTraceCtas = 8, kTraceSlots = 256;
+__device__ uint64_t* g_attn_trace = nullptr;
+#define ATTN_TRACE(slot)                                                                  \
+    do {                                                                                  \
+        uint64_t* tr_ = g_attn_trace;                                                     \
+        if (tr_ != nullptr && blockIdx.x < kTraceCtas && (slot) < kTraceSlots)            \
+            tr_[blockIdx.x * kTraceSlots + (slot)] = clock64();                           \
+    } while (0)
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -70,7 +82,7 @@ struct AttnParams {
     const float* prev_l;
     float* colsum;
     int layout;
-    int heads, n, chunk, chunks;
+    int heads, n, chunk, chunks, items;
     float qk_scale_log2;  // log2(e) / sqrt(E)
 };
 
@@ -90,30 +102,13 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     const uint32_t raw_u32 = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
 
+    // Persistent: CTA b processes items b, b + grid, ...  Every role walks the same item
+    // sequence and skips count-0 items identically, so ring / barrier phases run on two
+    // counters shared by all roles: `li` (live items) and `gb` (key blocks).
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int item = blockIdx.x;
-    const int c = item % p.chunks;
-    const int bh = item / p.chunks;
-    const int b = bh / p.heads, h = bh % p.heads;
     const bool dense = p.idx == nullptr;
-    const int cnt = dense ? p.n : p.counts[item];
-    const int row_base = p.layout == CSD_LAYOUT_BHNE ? bh * p.n : b * p.n;  // tensor-map row
-    const int col0 = p.layout == CSD_LAYOUT_BHNE ? 0 : h * E;
-    const int q_row0 = row_base + c * p.chunk;
-
-    if (cnt == 0) {  // pass base through (attention.cpp:169)
-        if (p.base != p.out && p.base != nullptr) {
-            for (int r = threadIdx.x; r < p.chunk * (E / 8); r += blockDim.x) {
-                const int row = r / (E / 8), v8 = r % (E / 8);
-                const int64_t off = tok_elem_off(p.layout, b, h, (int64_t)c * p.chunk + row,
-                                                 p.heads, p.n, E) + v8 * 8;
-                *reinterpret_cast<uint4*>(p.out + off) =
-                    *reinterpret_cast<const uint4*>(p.base + off);
-            }
-        }
-        return;
-    }
-    const int nblk = (cnt + 127) / 128;
+    const int items = p.items;
+    if (threadIdx.x == 0) ATTN_TRACE(0);
 
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
     uint64_t* bar_q = bars + 0;
@@ -124,7 +119,8 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     uint64_t* bar_s = bars + 9;    // [NT]
     uint64_t* bar_p = bars + 11;   // [NT]
     uint64_t* bar_o = bars + 13;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+    uint64_t* bar_qe = bars + 14;  // Q buffer free (all S MMAs of the item done)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
     if (threadIdx.x == 0) {
         mbar_init(bar_q, 1);
@@ -139,6 +135,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             mbar_init(bar_p + t, 128);
         }
         mbar_init(bar_o, 1);
+        mbar_init(bar_qe, 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<L::kTmemCols>(tmem_slot);
@@ -146,6 +143,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0) ATTN_TRACE(1);
     if (warp == 0 || warp == 2 || warp == 3) {
         // ------------------------------------------------------------ producers
         // TMA instructions issued by one warp are serialised lane by lane (~85 cycles each,
@@ -157,52 +155,69 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             tma_prefetch_desc(&tm_q);
             tma_prefetch_desc(dense ? &tm_k : &tm_kg);
             tma_prefetch_desc(dense ? &tm_v : &tm_vg);
-            mbar_arrive_expect_tx(bar_q, NT * L::kHalves * L::kStrip);
-            for (int t = 0; t < NT; ++t)
-                for (int hf = 0; hf < L::kHalves; ++hf)
-                    tma_load_2d(&tm_q, bar_q, smem + L::kQ + (t * L::kHalves + hf) * L::kStrip,
-                                col0 + hf * 64, q_row0 + t * 128);
         }
-        const int32_t* ids = dense ? nullptr : p.idx + (int64_t)item * p.k_max;
-        for (int j = 0; j < nblk; ++j) {
-            const int s = j & 1;
-            int32_t rows[4];
-            if (!dense) {
+        uint32_t gb = 0, li = 0;
+        for (int item = blockIdx.x; item < items; item += gridDim.x) {
+            const int cnt = dense ? p.n : p.counts[item];
+            if (cnt == 0) continue;
+            const int c = item % p.chunks, bh = item / p.chunks;
+            const int b = bh / p.heads, h = bh % p.heads;
+            const int row_base = p.layout == CSD_LAYOUT_BHNE ? bh * p.n : b * p.n;
+            const int col0 = p.layout == CSD_LAYOUT_BHNE ? 0 : h * E;
+            const int nblk = (cnt + 127) / 128;
+            if (warp == 0 && lane == 0) {
+                if (li > 0) mbar_wait(bar_qe, (li - 1) & 1);  // previous item's S MMAs done
+                ATTN_TRACE(2 + li);
+                mbar_arrive_expect_tx(bar_q, NT * L::kHalves * L::kStrip);
+                for (int t = 0; t < NT; ++t)
+                    for (int hf = 0; hf < L::kHalves; ++hf)
+                        tma_load_2d(&tm_q, bar_q, smem + L::kQ + (t * L::kHalves + hf) * L::kStrip,
+                                    col0 + hf * 64, row_base + c * p.chunk + t * 128);
+            }
+            const int32_t* ids = dense ? nullptr : p.idx + (int64_t)item * p.k_max;
+            for (int j = 0; j < nblk; ++j, ++gb) {
+                const int s = gb & 1;
+                int32_t rows[4];
+                if (!dense) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    int r = j * 128 + lane * 4 + i;
-                    r = r < cnt ? r : cnt - 1;  // pad with a valid row (masked in softmax)
-                    rows[i] = row_base + __ldg(ids + r);
+                    for (int i = 0; i < 4; ++i) {
+                        int r = j * 128 + lane * 4 + i;
+                        r = r < cnt ? r : cnt - 1;  // pad with a valid row (masked in softmax)
+                        rows[i] = row_base + __ldg(ids + r);
+                    }
                 }
-            }
-            // K_j -> ring slot s
-            if (j >= 2) mbar_wait(bar_ke + s, ((j >> 1) - 1) & 1);
-            if (warp == 0 && lane == 0) mbar_arrive_expect_tx(bar_kf + s, L::kKV);
-            uint8_t* kdst = smem + L::kK + s * L::kKV;
-            if (dense) {
-                if (warp == 0 && lane == 0)
+                // K_j -> ring slot s
+                if (gb >= 2) mbar_wait(bar_ke + s, ((gb >> 1) - 1) & 1);
+                if (warp == 0 && lane == 0) ATTN_TRACE(16 + gb);
+                if (warp == 0 && lane == 0) mbar_arrive_expect_tx(bar_kf + s, L::kKV);
+                uint8_t* kdst = smem + L::kK + s * L::kKV;
+                if (dense) {
+                    if (warp == 0 && lane == 0)
+                        for (int hf = 0; hf < L::kHalves; ++hf)
+                            tma_load_2d(&tm_k, bar_kf + s, kdst + hf * L::kStrip, col0 + hf * 64,
+                                        row_base + j * 128);
+                } else if (mine) {
                     for (int hf = 0; hf < L::kHalves; ++hf)
-                        tma_load_2d(&tm_k, bar_kf + s, kdst + hf * L::kStrip, col0 + hf * 64,
-                                    row_base + j * 128);
-            } else if (mine) {
-                for (int hf = 0; hf < L::kHalves; ++hf)
-                    tma_gather4(&tm_kg, bar_kf + s, kdst + hf * L::kStrip + lane * 512,
-                                col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
-            }
-            // V_j -> ring slot s
-            if (j >= 2) mbar_wait(bar_ve + s, ((j >> 1) - 1) & 1);
-            if (warp == 0 && lane == 0) mbar_arrive_expect_tx(bar_vf + s, L::kKV);
-            uint8_t* vdst = smem + L::kV + s * L::kKV;
-            if (dense) {
-                if (warp == 0 && lane == 0)
+                        tma_gather4(&tm_kg, bar_kf + s, kdst + hf * L::kStrip + lane * 512,
+                                    col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
+                }
+                // V_j -> ring slot s
+                if (gb >= 2) mbar_wait(bar_ve + s, ((gb >> 1) - 1) & 1);
+                if (warp == 0 && lane == 0) mbar_arrive_expect_tx(bar_vf + s, L::kKV);
+                uint8_t* vdst = smem + L::kV + s * L::kKV;
+                if (dense) {
+                    if (warp == 0 && lane == 0)
+                        for (int hf = 0; hf < L::kHalves; ++hf)
+                            tma_load_2d(&tm_v, bar_vf + s, vdst + hf * L::kStrip, col0 + hf * 64,
+                                        row_base + j * 128);
+                } else if (mine) {
                     for (int hf = 0; hf < L::kHalves; ++hf)
-                        tma_load_2d(&tm_v, bar_vf + s, vdst + hf * L::kStrip, col0 + hf * 64,
-                                    row_base + j * 128);
-            } else if (mine) {
-                for (int hf = 0; hf < L::kHalves; ++hf)
-                    tma_gather4(&tm_vg, bar_vf + s, vdst + hf * L::kStrip + lane * 512,
-                                col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
+                        tma_gather4(&tm_vg, bar_vf + s, vdst + hf * L::kStrip + lane * 512,
+                                    col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
+                }
+                if (warp == 0 && lane == 0) ATTN_TRACE(48 + gb);
             }
+            ++li;
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
@@ -211,8 +226,8 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             constexpr uint32_t idO = idesc_bf16(128, E, false, true);
             const uint32_t sQ = smem_u32(smem + L::kQ), sK = smem_u32(smem + L::kK);
             const uint32_t sV = smem_u32(smem + L::kV);
-            auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
-                const uint32_t kb = sK + (j & 1) * L::kKV;
+            auto issue_s = [&](int t, uint32_t g) {  // S_t = Q_t K_g^T
+                const uint32_t kb = sK + (g & 1) * L::kKV;
 #pragma unroll
                 for (int kk = 0; kk < E / 16; ++kk)
                     mma_bf16(tmem + t * 128,
@@ -221,38 +236,58 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                              kk > 0 ? 1u : 0u);
                 mma_commit(bar_s + t);
             };
-            auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j, P_t from TMEM
-                const uint32_t vb = sV + (j & 1) * L::kKV;
+            auto issue_pv = [&](int t, uint32_t g, bool acc) {  // O_t (+)= P_t V_g
+                const uint32_t vb = sV + (g & 1) * L::kKV;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
                     mma_bf16_ts(tmem + NT * 128 + t * E, tmem + t * 128 + kk * 8,
                                 desc_mnmajor_sw128(vb + kk * 2048, L::kStrip), idO,
-                                (j > 0 || kk > 0) ? 1u : 0u);
+                                (acc || kk > 0) ? 1u : 0u);
             };
-            mbar_wait(bar_q, 0);
-            mbar_wait(bar_kf, 0);
-            tc_fence_after();
-            for (int t = 0; t < NT; ++t) issue_s(t, 0);
-            mma_commit(bar_ke + 0);
-            for (int j = 0; j < nblk; ++j) {
-                const bool more = j + 1 < nblk;
-                for (int t = 0; t < NT; ++t) {
-                    mbar_wait(bar_p + t, j & 1);  // P_t(j) in TMEM, O_t rescaled
-                    if (t == 0) mbar_wait(bar_vf + (j & 1), (j >> 1) & 1);
-                    tc_fence_after();
-                    issue_pv(t, j);
-                    if (t == NT - 1) mma_commit(bar_ve + (j & 1));
-                    if (more) {
-                        if (t == 0) {
-                            mbar_wait(bar_kf + ((j + 1) & 1), ((j + 1) >> 1) & 1);
-                            tc_fence_after();
+            uint32_t gb = 0, li = 0;
+            for (int item = blockIdx.x; item < items; item += gridDim.x) {
+                const int cnt = dense ? p.n : p.counts[item];
+                if (cnt == 0) continue;
+                const int nblk = (cnt + 127) / 128;
+                // S_t(0) may overwrite S_t / P_t of the previous item: PV_t(last) was issued
+                // earlier and tcgen05 MMAs of one thread execute in order
+                mbar_wait(bar_q, li & 1);
+                ATTN_TRACE(8 + li);
+                mbar_wait(bar_kf + (gb & 1), (gb >> 1) & 1);
+                tc_fence_after();
+                ATTN_TRACE(80 + gb);
+                for (int t = 0; t < NT; ++t) issue_s(t, gb);
+                mma_commit(bar_ke + (gb & 1));
+                if (nblk == 1) mma_commit(bar_qe);
+                for (int j = 0; j < nblk; ++j) {
+                    const uint32_t g = gb + j;
+                    const bool more = j + 1 < nblk;
+                    for (int t = 0; t < NT; ++t) {
+                        // P_t(j) in TMEM and O_t rescaled; for j = 0 this also orders the
+                        // previous item's epilogue reads of O_t (same warps, program order)
+                        mbar_wait(bar_p + t, g & 1);
+                        if (t == 0) mbar_wait(bar_vf + (g & 1), (g >> 1) & 1);
+                        tc_fence_after();
+                        issue_pv(t, g, j > 0);
+                        if (t == NT - 1) mma_commit(bar_ve + (g & 1));
+                        if (more) {
+                            if (t == 0) {
+                                mbar_wait(bar_kf + ((g + 1) & 1), ((g + 1) >> 1) & 1);
+                                tc_fence_after();
+                                ATTN_TRACE(80 + g + 1);
+                            }
+                            issue_s(t, g + 1);  // in-order after PV_t(j): P_t consumed first
+                            if (t == NT - 1) {
+                                mma_commit(bar_ke + ((g + 1) & 1));
+                                if (j + 2 == nblk) mma_commit(bar_qe);
+                            }
                         }
-                        issue_s(t, j + 1);  // in-order after PV_t(j): P_t consumed first
-                        if (t == NT - 1) mma_commit(bar_ke + ((j + 1) & 1));
                     }
                 }
+                mma_commit(bar_o);
+                gb += nblk;
+                ++li;
             }
-            mma_commit(bar_o);
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ softmax / epilogue
@@ -266,172 +301,199 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         const uint32_t tS = tmem + lane_off + t * 128;
         const uint32_t tO = tmem + lane_off + NT * 128 + t * E;
         float* cs_part = reinterpret_cast<float*>(smem + L::kCs);
-        const int64_t tok = (int64_t)c * p.chunk + crow;
         const bool do_cs = p.colsum != nullptr;
-        float mpl = 0.f, inv_lp = 0.f;
-        if (do_cs && row_ok) {
-            const int64_t si = (int64_t)bh * p.n + tok;
-            mpl = p.prev_m[si] * kLog2e;
-            inv_lp = 1.0f / p.prev_l[si];
-        }
-        float m_run = -INFINITY, m_true = -INFINITY, l_run = 0.f;
         const float sl2 = p.qk_scale_log2;
-        for (int j = 0; j < nblk; ++j) {
-            mbar_wait(bar_s + t, j & 1);
-            tc_fence_after();
-            const int ncols = min(128, cnt - j * 128);
-            if (warp_ok) {
-                // S row in two 64-column halves (2 TMEM loads in flight, one wait each)
-                // fast path (uniform): every column and every row of this warp is live
-                const bool full = ncols == 128 && __all_sync(0xffffffffu, row_ok);
-                float mraw = -INFINITY;
-#pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    uint32_t sr[64];
-                    tmem_ld32(tS + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-                    tmem_ld32(tS + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-                    tmem_ld_wait();
-                    if (!full) {
-#pragma unroll
-                        for (int i = 0; i < 64; ++i)
-                            if (hf * 64 + i >= ncols) sr[i] = __float_as_uint(-INFINITY);
+        uint32_t gb = 0, li = 0;
+        for (int item = blockIdx.x; item < items; item += gridDim.x) {
+            const int cnt = dense ? p.n : p.counts[item];
+            const int c = item % p.chunks, bh = item / p.chunks;
+            const int b = bh / p.heads, h = bh % p.heads;
+            if (cnt == 0) {  // pass base through (attention.cpp:169)
+                if (p.base != p.out && p.base != nullptr) {
+                    for (int r = threadIdx.x - 128; r < p.chunk * (E / 8); r += 128 * NT) {
+                        const int row = r / (E / 8), v8 = r % (E / 8);
+                        const int64_t off = tok_elem_off(p.layout, b, h, (int64_t)c * p.chunk + row,
+                                                         p.heads, p.n, E) + v8 * 8;
+                        *reinterpret_cast<uint4*>(p.out + off) =
+                            *reinterpret_cast<const uint4*>(p.base + off);
                     }
+                }
+                continue;
+            }
+            const int nblk = (cnt + 127) / 128;
+            const int64_t tok = (int64_t)c * p.chunk + crow;
+            float mpl = 0.f, inv_lp = 0.f;
+            if (do_cs && row_ok) {
+                const int64_t si = (int64_t)bh * p.n + tok;
+                mpl = p.prev_m[si] * kLog2e;
+                inv_lp = 1.0f / p.prev_l[si];
+            }
+            float m_run = -INFINITY, m_true = -INFINITY, l_run = 0.f;
+            for (int j = 0; j < nblk; ++j) {
+                const uint32_t g = gb + j;
+                mbar_wait(bar_s + t, g & 1);
+                tc_fence_after();
+                if (lane == 0 && sw == 0) ATTN_TRACE(144 + g);
+                const int ncols = min(128, cnt - j * 128);
+                if (warp_ok) {
+                    // S row in two 64-column halves (2 TMEM loads in flight, one wait each)
+                    // fast path (uniform): every column and every row of this warp is live
+                    const bool full = ncols == 128 && __all_sync(0xffffffffu, row_ok);
+                    float mraw = -INFINITY;
 #pragma unroll
-                    for (int i = 0; i < 64; i += 2)
-                        mraw = fmax3(mraw, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
-                }
-                const float mx = row_ok ? mraw * sl2 : -INFINITY;  // sl2 > 0: max commutes
-                m_true = fmaxf(m_true, mx);
-                const bool need = mx > m_run + kRescaleThreshold;
-                const float alpha = need ? ex2_approx(m_run - mx) : 1.0f;
-                if (need) {
-                    m_run = mx;
-                    l_run *= alpha;
-                }
-                if (j > 0 && __any_sync(0xffffffffu, need)) {  // PV_t(j-1) done (bar_s order)
-#pragma unroll 1
-                    for (int oc = 0; oc < E / 32; ++oc) {
-                        uint32_t r[32];
-                        tmem_ld32(tO + oc * 32, r);
+                    for (int hf = 0; hf < 2; ++hf) {
+                        uint32_t sr[64];
+                        tmem_ld32(tS + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+                        tmem_ld32(tS + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
                         tmem_ld_wait();
+                        if (!full) {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-                        tmem_st32(tO + oc * 32, r);
+                            for (int i = 0; i < 64; ++i)
+                                if (hf * 64 + i >= ncols) sr[i] = __float_as_uint(-INFINITY);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 64; i += 2)
+                            mraw = fmax3(mraw, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
                     }
-                }
-                const float w = do_cs ? ex2_approx(m_run - mpl) * inv_lp : 0.f;
-                const float neg_m = row_ok ? -m_run : -INFINITY;  // dead rows -> p = 0
-#pragma unroll
-                for (int cc = 0; cc < 4; ++cc) {
-                    uint32_t sr[32];
-                    tmem_ld32(tS + cc * 32, sr);
-                    tmem_ld_wait();
-                    float pv[32];
-                    float part = 0.f;
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const float x = (full || cc * 32 + i < ncols) ? __uint_as_float(sr[i]) : -INFINITY;
-                        pv[i] = ex2_approx(fmaf(x, sl2, neg_m));
-                        part += pv[i];
+                    const float mx = row_ok ? mraw * sl2 : -INFINITY;  // sl2 > 0: max commutes
+                    m_true = fmaxf(m_true, mx);
+                    const bool need = mx > m_run + kRescaleThreshold;
+                    const float alpha = need ? ex2_approx(m_run - mx) : 1.0f;
+                    if (need) {
+                        m_run = mx;
+                        l_run *= alpha;
                     }
-                    l_run += part;
-                    // P_t (bf16 pairs) over S_t columns [16 cc, 16 cc + 16) — already read
+                    if (j > 0 && __any_sync(0xffffffffu, need)) {  // PV_t(j-1) done (bar_s order)
+#pragma unroll 1
+                        for (int oc = 0; oc < E / 32; ++oc) {
+                            uint32_t r[32];
+                            tmem_ld32(tO + oc * 32, r);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+                            tmem_st32(tO + oc * 32, r);
+                        }
+                    }
+                    const float w = do_cs ? ex2_approx(m_run - mpl) * inv_lp : 0.f;
+                    const float neg_m = row_ok ? -m_run : -INFINITY;  // dead rows -> p = 0
+#pragma unroll
+                    for (int cc = 0; cc < 4; ++cc) {
+                        uint32_t sr[32];
+                        tmem_ld32(tS + cc * 32, sr);
+                        tmem_ld_wait();
+                        float pv[32];
+                        float part = 0.f;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const float x = (full || cc * 32 + i < ncols) ? __uint_as_float(sr[i]) : -INFINITY;
+                            pv[i] = ex2_approx(fmaf(x, sl2, neg_m));
+                            part += pv[i];
+                        }
+                        l_run += part;
+                        // P_t (bf16 pairs) over S_t columns [16 cc, 16 cc + 16) — already read
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(pv[2 * q], pv[2 * q + 1]);
+                        tmem_st16(tS + cc * 16, pk);
+                        if (do_cs) {
+                            // transpose-reduce the warp's 32x32 block: lane ends with column `lane`
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) pv[i] *= w;
+#pragma unroll
+                            for (int wd = 16; wd >= 1; wd >>= 1) {
+                                const bool upper = (lane & wd) != 0;
+#pragma unroll
+                                for (int i = 0; i < wd; ++i) {
+                                    const float send = upper ? pv[i] : pv[i + wd];
+                                    const float keep = upper ? pv[i + wd] : pv[i];
+                                    pv[i] = keep + __shfl_xor_sync(0xffffffffu, send, wd);
+                                }
+                            }
+                            cs_part[((g & 1) * 4 * NT + sw) * 128 + cc * 32 + lane] = pv[0];
+                        }
+                    }
+                } else {
+                    // rows past the chunk: zero P so the padded MMA rows stay finite
                     uint32_t pk[16];
 #pragma unroll
-                    for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(pv[2 * q], pv[2 * q + 1]);
-                    tmem_st16(tS + cc * 16, pk);
-                    if (do_cs) {
-                        // transpose-reduce the warp's 32x32 block: lane ends with column `lane`
+                    for (int q = 0; q < 16; ++q) pk[q] = 0u;
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) pv[i] *= w;
-#pragma unroll
-                        for (int wd = 16; wd >= 1; wd >>= 1) {
-                            const bool upper = (lane & wd) != 0;
-#pragma unroll
-                            for (int i = 0; i < wd; ++i) {
-                                const float send = upper ? pv[i] : pv[i + wd];
-                                const float keep = upper ? pv[i + wd] : pv[i];
-                                pv[i] = keep + __shfl_xor_sync(0xffffffffu, send, wd);
-                            }
-                        }
-                        cs_part[((j & 1) * 4 * NT + sw) * 128 + cc * 32 + lane] = pv[0];
+                    for (int cc = 0; cc < 4; ++cc) tmem_st16(tS + cc * 16, pk);
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(bar_p + t);
+                if (lane == 0 && sw == 0) ATTN_TRACE(168 + g);
+                if (do_cs) {
+                    named_bar_sync(1, 128 * NT);
+                    const int st = sw * 32 + lane;
+                    if (st < 128 && st < ncols) {
+                        float s = 0.f;
+                        for (int wsl = 0; wsl < 4 * NT; ++wsl)
+                            if (wsl * 32 < p.chunk) s += cs_part[((g & 1) * 4 * NT + wsl) * 128 + st];
+                        p.colsum[((int64_t)bh * p.chunks + c) * p.n + j * 128 + st] = s;
                     }
                 }
-            } else {
-                // rows past the chunk: zero P so the padded MMA rows stay finite
-                uint32_t pk[16];
-#pragma unroll
-                for (int q = 0; q < 16; ++q) pk[q] = 0u;
-#pragma unroll
-                for (int cc = 0; cc < 4; ++cc) tmem_st16(tS + cc * 16, pk);
             }
-            tmem_st_wait();
-            tc_fence_before();
-            mbar_arrive(bar_p + t);
-            if (do_cs) {
-                named_bar_sync(1, 128 * NT);
-                const int st = sw * 32 + lane;
-                if (st < 128 && st < ncols) {
-                    float s = 0.f;
-                    for (int wsl = 0; wsl < 4 * NT; ++wsl)
-                        if (wsl * 32 < p.chunk) s += cs_part[((j & 1) * 4 * NT + wsl) * 128 + st];
-                    p.colsum[((int64_t)bh * p.chunks + c) * p.n + j * 128 + st] = s;
-                }
+            // ------------------------------------------------------------ epilogue
+            const int64_t off = tok_elem_off(p.layout, b, h, tok, p.heads, p.n, E);
+            uint4 bpre[E / 8];  // prefetch base while the last P.V runs
+            const bool has_base = p.base != nullptr;
+            if (warp_ok && row_ok && has_base) {
+                const uint4* bp = reinterpret_cast<const uint4*>(p.base + off);
+#pragma unroll
+                for (int q = 0; q < E / 8; ++q) bpre[q] = __ldg(bp + q);
             }
-        }
-        // ------------------------------------------------------------ epilogue
-        const int64_t off = tok_elem_off(p.layout, b, h, tok, p.heads, p.n, E);
-        uint4 bpre[E / 8];  // prefetch base while the last P.V runs
-        const bool has_base = p.base != nullptr;
-        if (warp_ok && row_ok && has_base) {
-            const uint4* bp = reinterpret_cast<const uint4*>(p.base + off);
+            mbar_wait(bar_o, li & 1);
+            tc_fence_after();
+            if (lane == 0 && sw == 0) ATTN_TRACE(240 + li);
+            if (warp_ok) {
+                const float inv_l = 1.0f / l_run;
 #pragma unroll
-            for (int q = 0; q < E / 8; ++q) bpre[q] = __ldg(bp + q);
-        }
-        mbar_wait(bar_o, 0);
-        tc_fence_after();
-        if (warp_ok) {
-            const float inv_l = 1.0f / l_run;
+                for (int oc = 0; oc < E / 32; ++oc) {
+                    uint32_t r[32];
+                    tmem_ld32(tO + oc * 32, r);
+                    tmem_ld_wait();
+                    if (row_ok) {
+                        float o[32];
 #pragma unroll
-            for (int oc = 0; oc < E / 32; ++oc) {
-                uint32_t r[32];
-                tmem_ld32(tO + oc * 32, r);
-                tmem_ld_wait();
-                if (row_ok) {
-                    float o[32];
+                        for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r[i]) * inv_l;
+                        if (has_base) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r[i]) * inv_l;
-                    if (has_base) {
+                            for (int q = 0; q < 4; ++q) {
+                                const __nv_bfloat162* b2 =
+                                    reinterpret_cast<const __nv_bfloat162*>(&bpre[oc * 4 + q]);
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const float2 f = __bfloat1622float2(b2[u]);
+                                    o[q * 8 + 2 * u] = f.x + p.scale * o[q * 8 + 2 * u];
+                                    o[q * 8 + 2 * u + 1] = f.y + p.scale * o[q * 8 + 2 * u + 1];
+                                }
+                            }
+                        }
+                        uint4* dp = reinterpret_cast<uint4*>(p.out + off + oc * 32);
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const __nv_bfloat162* b2 =
-                                reinterpret_cast<const __nv_bfloat162*>(&bpre[oc * 4 + q]);
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                const float2 f = __bfloat1622float2(b2[u]);
-                                o[q * 8 + 2 * u] = f.x + p.scale * o[q * 8 + 2 * u];
-                                o[q * 8 + 2 * u + 1] = f.y + p.scale * o[q * 8 + 2 * u + 1];
-                            }
+                            uint4 v;
+                            v.x = pack_bf16x2(o[q * 8 + 0], o[q * 8 + 1]);
+                            v.y = pack_bf16x2(o[q * 8 + 2], o[q * 8 + 3]);
+                            v.z = pack_bf16x2(o[q * 8 + 4], o[q * 8 + 5]);
+                            v.w = pack_bf16x2(o[q * 8 + 6], o[q * 8 + 7]);
+                            dp[q] = v;
                         }
                     }
-                    uint4* dp = reinterpret_cast<uint4*>(p.out + off + oc * 32);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        uint4 v;
-                        v.x = pack_bf16x2(o[q * 8 + 0], o[q * 8 + 1]);
-                        v.y = pack_bf16x2(o[q * 8 + 2], o[q * 8 + 3]);
-                        v.z = pack_bf16x2(o[q * 8 + 4], o[q * 8 + 5]);
-                        v.w = pack_bf16x2(o[q * 8 + 6], o[q * 8 + 7]);
-                        dp[q] = v;
-                    }
+                }
+                if (row_ok && p.row_max != nullptr) {
+                    const int64_t si = (int64_t)bh * p.n + tok;
+                    p.row_max[si] = m_true * kLn2;
+                    p.exp_sum[si] = l_run * exp2f(m_run - m_true);
                 }
             }
-            if (row_ok && p.row_max != nullptr) {
-                const int64_t si = (int64_t)bh * p.n + tok;
-                p.row_max[si] = m_true * kLn2;
-                p.exp_sum[si] = l_run * exp2f(m_run - m_true);
-            }
+            if (lane == 0 && sw == 0) ATTN_TRACE(248 + li);
+            tc_fence_before();  // O reads ordered before the next item's bar_p arrive
+            gb += nblk;
+            ++li;
         }
     }
     tc_fence_before();
@@ -507,6 +569,7 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
     p.n = (int)a.n;
     p.chunk = (int)a.chunk;
     p.chunks = (int)(a.n / a.chunk);
+    p.items = (int)(a.batch * a.heads * p.chunks);
     p.qk_scale_log2 = kLog2e / std::sqrt((float)E);
     auto kern = k_attn_tc<E, NT>;
     static bool attr_done = false;  // once per instantiation (keeps graph capture clean)
@@ -516,7 +579,14 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
         if (err != cudaSuccess) return err;
         attr_done = true;
     }
-    const unsigned grid = (unsigned)(a.batch * a.heads * p.chunks);
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    // persistent: one CTA per SM (smem-limited), items strided over the grid
+    const unsigned grid = (unsigned)std::min<int64_t>(p.items, sms);
     kern<<<grid, L::kThreads, L::kSmemAlloc, s>>>(tq, tk, tv, tkg, tvg, p);
     return cudaGetLastError();
 }
@@ -531,3 +601,10 @@ cudaError_t attn_tc(const AttnTcArgs& a, cudaStream_t s) {
 
 }  // namespace dev
 }  // namespace csd
+
+// Debug only (scripts/attn_trace.py): point the attention kernels' timeline buffer at a
+// device array of kTraceCtas * kTraceSlots uint64 (nullptr disables tracing).
+extern "C" int csd_debug_set_attn_trace(void* dev_buf) {
+    uint64_t* p = static_cast<uint64_t*>(dev_buf);
+    return cudaMemcpyToSymbol(csd::dev::g_attn_trace, &p, sizeof(p)) == cudaSuccess ? 0 : 7;
+}

@@ -35,6 +35,20 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
+// Non-blocking probe: true once the phase with `parity` has completed.
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     asm volatile(
@@ -74,6 +88,17 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* m, uint64_t* bar,
         " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
+}
+// L2 prefetch of one 2D box (no smem, no barrier).
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+// L2 prefetch of a contiguous byte range (16-byte aligned start, size multiple of 16).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 // 2D gather4: four rows (r0..r3) of one box-width column strip, stored as
 // four consecutive box rows at dst.
@@ -184,6 +209,26 @@ __device__ __forceinline__ void regs_dec() {
 template <uint32_t kRegs>
 __device__ __forceinline__ void regs_inc() {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+// 2^x on the FMA pipe (x <= 0 expected; clamped at -126 so the exponent add never wraps): round-to-nearest split
+// x = n + f, f in [-0.5, 0.5], degree-3 minimax for 2^f (rel. err < 2e-4, far below the
+// bf16 rounding of P), exponent added with an integer shift.  Two values per call so the
+// arithmetic runs as paired f32x2 instructions (FADD2 / FFMA2).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -126.f);
+    x.y = fmaxf(x.y, -126.f);
+    const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+    const float2 t = __fadd2_rn(x, magic);
+    const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), x);
+    float2 q = __ffma2_rn(f, make_float2(0.05489881f, 0.05489881f),
+                          make_float2(0.24193298f, 0.24193298f));
+    q = __ffma2_rn(q, f, make_float2(0.69324847f, 0.69324847f));
+    q = __ffma2_rn(q, f, make_float2(0.99997654f, 0.99997654f));
+    float2 y;
+    y.x = __int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23));
+    y.y = __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23));
+    return y;
 }
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;

@@ -35,7 +35,7 @@ k_bench(const __grid_constant__ CUtensorMap tile_map, const __grid_constant__ CU
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(full + s, mode == 5 ? 128 : mode == 6 ? 65 : 1);
+            mbar_init(full + s, mode == 5 ? 128 : mode == 6 ? 65 : mode == 7 ? blockDim.x : 1);
             mbar_init(empty + s, blockDim.x / 32);
         }
         fence_barrier_init();
@@ -98,6 +98,30 @@ k_bench(const __grid_constant__ CUtensorMap tile_map, const __grid_constant__ CU
                 }
                 asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)));
             }
+        } else if (mode >= 8 && mode <= 10) {
+            // raw 1D bulk copies of contiguous row segments (no swizzle): mode 8 = 128 B x 128
+            // rows, 9 = 256 B x 64 rows, 10 = 1 KB x 16 rows (16 KB per stage in all cases)
+            const int seg = mode == 8 ? 128 : mode == 9 ? 256 : 1024;
+            const int nseg = kBlk / seg;
+            if (threadIdx.x == 0) mbar_arrive_expect_tx(full + s, kBlk);
+            __syncthreads();
+            for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+                const __nv_bfloat16* src = base + (size_t)rows[rbase + i] * ld;
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %3, [%2];"
+                    ::"r"(smem_u32(dst + i * seg)), "l"(src), "r"(smem_u32(full + s)), "r"(seg) : "memory");
+            }
+        } else if (mode == 7) {
+            // row-coalesced cp.async: 8 consecutive lanes fetch one row's 128 B (8 x 16 B,
+            // swizzled destinations); each warp instruction covers 4 rows
+            const int nthr = blockDim.x;
+            for (int idx = threadIdx.x; idx < 128 * 8; idx += nthr) {
+                const int row = idx >> 3, c = idx & 7;
+                const uint8_t* src = reinterpret_cast<const uint8_t*>(base + (size_t)rows[rbase + row] * ld) + c * 16;
+                const uint32_t d = smem_u32(dst) + sw128_offset(row, c);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src));
+            }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)));
         } else {  // mode 5
             // 128 threads x 8 x 16 B; row = tid, chunks 0..7 swizzled
             const int row = threadIdx.x;
@@ -119,6 +143,7 @@ k_bench(const __grid_constant__ CUtensorMap tile_map, const __grid_constant__ CU
 }
 
 int main(int argc, char** argv) {
+    const int g_ctas = getenv("CTAS") ? atoi(getenv("CTAS")) : 148;
     const int rows_total = 1 << 17, cols = 64;  // 128 B rows (one 64-column strip)
     const int ld = 3072;                         // real pitch: rows of a [F, 3072] weight
     const size_t elems = (size_t)rows_total * ld;
@@ -169,6 +194,15 @@ int main(int argc, char** argv) {
         {"tma gather4 16 warps x2 (random, L2)", 3, rows_l2, 512},
         {"tma gather4 8 warps x4 (random, DRAM)", 3, rows, 256},
         {"tma gather4 16 warps x2 (random, DRAM)", 3, rows, 512},
+        {"bulk 1D 128 B segments (L2)", 8, rows_l2, 128},
+        {"bulk 1D 256 B segments (L2)", 9, rows_l2, 128},
+        {"bulk 1D 1 KB segments (L2)", 10, rows_l2, 128},
+        {"bulk 1D 256 B segments (DRAM)", 9, rows, 128},
+        {"bulk 1D 1 KB segments (DRAM)", 10, rows, 128},
+        {"cp.async row-coalesced 128 thr (L2)", 7, rows_l2, 128},
+        {"cp.async row-coalesced 256 thr (L2)", 7, rows_l2, 256},
+        {"cp.async row-coalesced 512 thr (L2)", 7, rows_l2, 512},
+        {"cp.async row-coalesced 256 thr (DRAM)", 7, rows, 256},
         {"cp.async 128 thr (random, L2)", 5, rows_l2, 128},
         {"cp.async 128 thr (random, DRAM)", 5, rows, 128},
         {"mixed g4 4 warps + cp.async 64 thr (L2)", 6, rows_l2, 256},
@@ -182,12 +216,12 @@ int main(int argc, char** argv) {
             cudaEventCreate(&a);
             cudaEventCreate(&b);
             cudaEventRecord(a);
-            k_bench<<<148, cs.threads, smem>>>(tm, tg, d, ld, r, rows_total, iters, mode, sink);
+            k_bench<<<g_ctas, cs.threads, smem>>>(tm, tg, d, ld, r, rows_total, iters, mode, sink);
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             float ms;
             cudaEventElapsedTime(&ms, a, b);
-            const double bytes = 148.0 * iters * kBlk;
+            const double bytes = (double)g_ctas * iters * kBlk;
             if (rep) printf("%-38s %8.3f ms  %8.1f GB/s  (%.0f ns per 16 KB block per SM)\n", cs.name, ms,
                             bytes / (ms * 1e-3) / 1e9, ms * 1e6 / iters);
         }

@@ -221,12 +221,14 @@ def test_check_block_trajectory_bit_exact(ops, golden):
 
 
 # ------------------------------------------------------------------ PROD-mode attention (tcgen05)
-@pytest.mark.parametrize("e,chunk,n,layout", [(128, 192, 768, 0), (64, 64, 512, 0),
-                                              (128, 128, 640, 1), (64, 192, 384, 1),
-                                              (128, 256, 512, 0)])
-def test_prod_sparse_delta_attention(ops, port, e, chunk, n, layout):
+# h x (n / chunk) > 148 cases run several work items per persistent CTA
+@pytest.mark.parametrize("e,chunk,n,layout,h", [(128, 192, 768, 0, 3), (64, 64, 512, 0, 3),
+                                                (128, 128, 640, 1, 3), (64, 192, 384, 1, 3),
+                                                (128, 256, 512, 0, 3), (128, 192, 4608, 1, 8),
+                                                (64, 64, 2048, 0, 7)])
+def test_prod_sparse_delta_attention(ops, port, e, chunk, n, layout, h):
     rng = np.random.default_rng(e * 7 + chunk + n)
-    b, h = 1, 3
+    b = 1
     shape = (b, h, n, e) if layout == 0 else (b, n, h, e)
     q, k, v, base = (port.gaussian(300 + i, shape) for i in range(4))
     q16, k16, v16, b16 = (bf(a) for a in (q, k, v, base))
@@ -257,9 +259,10 @@ def test_prod_sparse_delta_attention(ops, port, e, chunk, n, layout):
                     assert np.array_equal(got[0, hh, c * chunk:(c + 1) * chunk], to_bhne(b16)[0, hh, c * chunk:(c + 1) * chunk])
 
 
-@pytest.mark.parametrize("e,chunk,n", [(128, 192, 768), (64, 64, 512), (128, 128, 384)])
-def test_prod_dense_and_colsum_attention(ops, port, e, chunk, n):
-    q, k, v = (bf(port.gaussian(400 + i, (1, 2, n, e))) for i in range(3))
+@pytest.mark.parametrize("e,chunk,n,h", [(128, 192, 768, 2), (64, 64, 512, 2), (128, 128, 384, 2),
+                                         (64, 64, 1024, 10)])
+def test_prod_dense_and_colsum_attention(ops, port, e, chunk, n, h):
+    q, k, v = (bf(port.gaussian(400 + i, (1, h, n, e))) for i in range(3))
     want_o, want_cs, (wm, wl) = port.column_sum_attention(q, k, v, None, chunk)
     qt, kt, vt = (T(a, torch.bfloat16) for a in (q, k, v))
     o = ops.dense_attention(qt, kt, vt)
