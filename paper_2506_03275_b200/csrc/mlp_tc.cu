@@ -12,6 +12,8 @@
 // Both kernels: warp 0 = TMA producer (x / delta tiles + gather4 of weight rows),
 // warp 1 = single-thread tcgen05.mma issuer, warps 4.. = TMEM -> register epilogue.
 // 4-stage smem ring (48 KB per stage), fp32 accumulators in TMEM.
+#include <algorithm>
+
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -28,7 +30,17 @@ using namespace csd::tc;
 bool make_map_bf16(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows,
                    uint64_t pitch_elems, uint32_t box_rows);
 
-constexpr int kMlpStages = 2;  // 2 x 48 KB: two CTAs per SM (grid tails, TMA overlap)
+// Debug timeline (scripts/mlp_trace.py): CTAs with blockIdx.y == 0 and blockIdx.x < 8
+// record clock64() at fixed slots when the pointer is set.
+__device__ uint64_t* g_mlp_trace = nullptr;
+#define MLP_TRACE(slot)                                                                   \
+    do {                                                                                  \
+        uint64_t* tr_ = g_mlp_trace;                                                      \
+        if (tr_ != nullptr && blockIdx.y == 0 && blockIdx.x < 8 && (slot) < 256)          \
+            tr_[blockIdx.x * 256 + (slot)] = clock64();                                   \
+    } while (0)
+
+constexpr int kMlpStages = 4;  // 4 x 48 KB: one CTA per SM, deep enough to cover L2 latency
 constexpr uint32_t kTile = 128 * 128;  // 128 rows x 64 bf16 (128 B) = 16 KB
 
 template <int NT>
@@ -43,9 +55,12 @@ struct MlpLayout {
 };
 
 struct MlpParams {
+    const __nv_bfloat16* w1;  // gathered rows are staged with cp.async from these
+    const __nv_bfloat16* w2;
     const int32_t* idx;
     const int32_t* counts;
     int k_max, k_pad;
+    int tn_width;  // neurons per up-projection tile (multiple of 16, <= kUpMaxTN)
     const float* b1;
     __nv_bfloat16* act_cm;
     __nv_bfloat16* delta;
@@ -80,7 +95,7 @@ __device__ __forceinline__ void residual32(const MlpParams& p, int64_t row, int 
 
 template <int NT>
 __device__ __forceinline__ void mlp_setup(uint8_t* smem, uint64_t*& full, uint64_t*& empty,
-                                          uint64_t*& done, uint32_t& tmem) {
+                                          uint64_t*& done, uint32_t& tmem, uint32_t full_count) {
     using L = MlpLayout<NT>;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
     full = bars;
@@ -89,7 +104,7 @@ __device__ __forceinline__ void mlp_setup(uint8_t* smem, uint64_t*& full, uint64
     uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 2 * kMlpStages + 1);
     if (threadIdx.x == 0) {
         for (int s = 0; s < kMlpStages; ++s) {
-            mbar_init(full + s, 1);
+            mbar_init(full + s, full_count);
             mbar_init(empty + s, 1);
         }
         mbar_init(done, 1);
@@ -103,129 +118,254 @@ __device__ __forceinline__ void mlp_setup(uint8_t* smem, uint64_t*& full, uint64
 }
 
 // ------------------------------------------------------------------ up projection
+// Tile = (chunk z, neuron tile tn of TN = p.tn_width neurons; TN is picked on the host so
+// that all tiles run in ONE wave on 148 SMs, e.g. FLUX 860 -> 6 x 144).  MMA: M = chunk
+// rows (NT x 128), N = TN, K = D.  Stage = x tile (TMA) + TN gathered W1 k-slices (cp.async).
+constexpr int kUpMaxTN = 192;
 template <int NT>
-__global__ void __launch_bounds__(MlpLayout<NT>::kThreads, 2)
-k_smlp_up(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w1g,
-          const MlpParams p) {
-    using L = MlpLayout<NT>;
+struct UpLayout {
+    static constexpr uint32_t kStageMax = NT * kTile + kUpMaxTN * 128;
+    static constexpr uint32_t kThreads = 128 + 128 * NT;
+    static constexpr uint32_t kBarBytes = 128 + 1024 + 1024;  // barriers, ids, biases
+    static constexpr uint32_t kMaxSmem = 227 * 1024;
+    static constexpr uint32_t kTmemCols = NT * kUpMaxTN <= 256 ? 256 : 512;
+    __host__ __device__ static constexpr uint32_t stage_bytes(int tn) {
+        return NT * kTile + (uint32_t)tn * 128u;
+    }
+    __host__ __device__ static constexpr int stages(int tn) {
+        return (4 * stage_bytes(tn) + kBarBytes + 1024 <= kMaxSmem) ? 4 : 3;
+    }
+    __host__ __device__ static constexpr uint32_t alloc(int tn) {
+        return stages(tn) * stage_bytes(tn) + kBarBytes + 1024;
+    }
+};
+
+template <int NT>
+__global__ void __launch_bounds__(UpLayout<NT>::kThreads, 1)
+k_smlp_up(const __grid_constant__ CUtensorMap tm_x, const MlpParams p) {
+    using L = UpLayout<NT>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int z = blockIdx.y, tn = blockIdx.x;
+    const int z = blockIdx.y, tn = blockIdx.x, TN = p.tn_width;
     const int cnt = p.counts[z];
-    if (tn * 128 >= cnt) return;
+    const int n0 = tn * TN;  // first neuron slot of this tile
     const int b = z / p.chunks, c = z % p.chunks;
     const int x_row0 = b * p.n + c * p.chunk;
     const int kblocks = p.d / 64;
+    const int nst = L::stages(TN);
+    const uint32_t sbytes = L::stage_bytes(TN);
     const int32_t* ids = p.idx + (int64_t)z * p.k_max;
+    const int nval = max(0, min(TN, cnt - n0));  // live neurons in this tile
+    // delta rows of this chunk: [z * chunk + r][k_pad]
+    __nv_bfloat16* drow0 = p.delta + (int64_t)z * p.chunk * p.k_pad;
 
-    uint64_t *full, *empty, *done;
-    uint32_t tmem;
-    mlp_setup<NT>(smem, full, empty, done, tmem);
+    uint8_t* barp = smem + nst * sbytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(barp);
+    uint64_t* empty = full + 4;
+    uint64_t* done = full + 8;
+    uint32_t* slot = reinterpret_cast<uint32_t*>(full + 9);
+    int32_t* s_ids = reinterpret_cast<int32_t*>(barp + 128);
+    float* s_b1 = reinterpret_cast<float*>(barp + 128 + 1024);
+    constexpr int kCopyThreads = L::kThreads - 32;
+    if (nval == 0) {
+        // no live neuron: this tile's delta columns are zero (the down GEMM reads them)
+        for (int idx = threadIdx.x; idx < p.chunk * (TN / 8); idx += blockDim.x) {
+            const int r = idx / (TN / 8), pc = idx - r * (TN / 8);
+            *reinterpret_cast<uint4*>(drow0 + (int64_t)r * p.k_pad + n0 + pc * 8) = make_uint4(0, 0, 0, 0);
+        }
+        return;
+    }
+    if (threadIdx.x == 0) {
+        MLP_TRACE(0);
+        for (int s = 0; s < nst; ++s) {
+            // the x-tile expect_tx arrival + one cp.async-tracking arrival per copy thread
+            mbar_init(full + s, 1 + kCopyThreads);
+            mbar_init(empty + s, 1);
+        }
+        mbar_init(done, 1);
+        fence_barrier_init();
+    }
+    for (int i = threadIdx.x; i < TN; i += blockDim.x) {
+        const int nn = n0 + i;
+        const int neuron = ids[nn < cnt ? nn : cnt - 1];  // pad: a valid row (column unused)
+        s_ids[i] = neuron;
+        s_b1[i] = p.b1[neuron];
+    }
+    if (warp == 1) tmem_alloc<L::kTmemCols>(slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *slot;
+    if (threadIdx.x == 0) MLP_TRACE(1);
 
-    if (warp == 0 || warp == 2 || warp == 3) {
-        // producers: warp 0 issues the x tiles; the 32 W1-row gather4s per stage are spread
-        // over warps 0/2/3 (one warp's TMA issue is serialised, scripts/gather_bench.cu)
-        const int pw = warp == 0 ? 0 : warp - 1;
-        const bool mine = (lane % 3) == pw;
-        int32_t rows[4];
+    if (warp != 1) {
+        // Producers = every warp but the MMA warp (the epilogue warps are idle until the
+        // accumulator is final).  Warp 0 lane 0 issues the x tiles by TMA; the TN gathered
+        // W1 rows of each stage are staged with cp.async, 16-byte pieces, the 8 pieces of a
+        // row's 128-byte k-slice on consecutive threads (scripts/gather_bench2.cu: ~2.6x
+        // TMA tile::gather4's per-SM rate).  A thread's rows are fixed for the whole K loop.
+        const int ct = threadIdx.x < 32 ? threadIdx.x : threadIdx.x - 32;
+        constexpr int kPer = (kUpMaxTN * 8 + kCopyThreads - 1) / kCopyThreads;
+        const char* src[kPer];
+        uint32_t dso[kPer];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            int nn = tn * 128 + lane * 4 + i;
-            rows[i] = ids[nn < cnt ? nn : cnt - 1];
+        for (int i = 0; i < kPer; ++i) {
+            const int idx = ct + i * kCopyThreads;
+            const int row = idx >> 3, c8 = idx & 7;
+            const bool ok = row < TN;
+            src[i] = reinterpret_cast<const char*>(p.w1 + (int64_t)s_ids[ok ? row : 0] * p.d) + c8 * 16;
+            dso[i] = ok ? (uint32_t)(NT * kTile + row * 128 + ((c8 ^ (row & 7)) << 4)) : 0xffffffffu;
         }
-        if (warp == 0 && lane == 0) {
-            tma_prefetch_desc(&tm_x);
-            tma_prefetch_desc(&tm_w1g);
-        }
+        if (warp == 0 && lane == 0) tma_prefetch_desc(&tm_x);
+        const uint32_t s0 = smem_u32(smem);
         for (int kb = 0; kb < kblocks; ++kb) {
-            const int s = kb % kMlpStages;
-            if (kb >= kMlpStages) mbar_wait(empty + s, ((kb / kMlpStages) - 1) & 1);
-            if (warp == 0 && lane == 0) {
-                mbar_arrive_expect_tx(full + s, (NT + 1) * kTile);
-                for (int t = 0; t < NT; ++t)
-                    tma_load_2d(&tm_x, full + s, smem + L::kA + (s * NT + t) * kTile, kb * 64,
-                                x_row0 + t * 128);
+            const int s = kb % nst;
+            if (kb == nst && warp == 4) {
+                // warm L2 with this tile's activation-cache rows (the epilogue's input)
+                const __nv_bfloat16* cache_z = p.act_cm + (int64_t)z * p.f * p.chunk;
+                for (int n = lane; n < nval; n += 32)
+                    bulk_prefetch_l2(cache_z + (int64_t)s_ids[n] * p.chunk, (uint32_t)p.chunk * 2u);
             }
-            if (mine)
-                tma_gather4(&tm_w1g, full + s, smem + L::kB + s * kTile + lane * 512, kb * 64,
-                            rows[0], rows[1], rows[2], rows[3]);
+            if (kb >= nst) mbar_wait(empty + s, ((kb / nst) - 1) & 1);
+            if (warp == 0 && lane == 0) {
+                MLP_TRACE(2 + kb);
+                mbar_arrive_expect_tx(full + s, NT * kTile);
+                for (int t = 0; t < NT; ++t)
+                    tma_load_2d(&tm_x, full + s, smem + s * sbytes + t * kTile, kb * 64, x_row0 + t * 128);
+            }
+#pragma unroll
+            for (int i = 0; i < kPer; ++i)
+                if (dso[i] != 0xffffffffu)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s0 + s * sbytes + dso[i]),
+                                 "l"(src[i] + kb * 128) : "memory");
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)) : "memory");
         }
-    } else if (warp == 1) {
+    }
+    if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t id = idesc_bf16(128, 128, false, false);
-            const uint32_t sA = smem_u32(smem + L::kA), sB = smem_u32(smem + L::kB);
+            const uint32_t id = idesc_bf16(128, (uint32_t)TN, false, false);
+            const uint32_t s0 = smem_u32(smem);
             for (int kb = 0; kb < kblocks; ++kb) {
-                const int s = kb % kMlpStages;
-                mbar_wait(full + s, (kb / kMlpStages) & 1);
+                const int s = kb % nst;
+                mbar_wait(full + s, (kb / nst) & 1);
+                fence_proxy_async_smem();  // cp.async (generic proxy) data -> tcgen05 reads
                 tc_fence_after();
+                MLP_TRACE(64 + kb);
+                const uint32_t sa = s0 + s * sbytes, sb = sa + NT * kTile;
                 for (int t = 0; t < NT; ++t) {
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)
-                        mma_bf16(tmem + t * 128, desc_kmajor_sw128(sA + (s * NT + t) * kTile + kk * 32),
-                                 desc_kmajor_sw128(sB + s * kTile + kk * 32), id,
-                                 (kb > 0 || kk > 0) ? 1u : 0u);
+                        mma_bf16(tmem + t * kUpMaxTN, desc_kmajor_sw128(sa + t * kTile + kk * 32),
+                                 desc_kmajor_sw128(sb + kk * 32), id, (kb > 0 || kk > 0) ? 1u : 0u);
                 }
                 mma_commit(empty + s);
             }
             mma_commit(done);
         }
     } else if (warp >= 4) {
+        // Staged epilogue in the (now idle) stage ring:
+        //   act tile   [TN neurons][chunk rows] bf16: a selected neuron's chunk-major cache row
+        //              is contiguous (chunk x 2 B): coalesced 16-byte cp.async in / stores out;
+        //   delta tile [chunk rows][TN] bf16, row pitch TN * 2 + 16 B (bank-conflict free),
+        //              written out row-contiguously.
+        // Thread = chunk row: a warp's smem accesses hit consecutive rows.
         const int sw = warp - 4, t = sw >> 2, quad = warp & 3;
         const int r = t * 128 + quad * 32 + lane;  // row within the chunk
         const bool row_ok = r < p.chunk;
-        // stage this tile's neuron ids and biases in smem while the MMAs run, so the
-        // epilogue's cache read-modify-write has no dependent global loads
-        int32_t* s_ids = reinterpret_cast<int32_t*>(smem + L::kBar + 128);
-        float* s_b1 = reinterpret_cast<float*>(smem + L::kBar + 128 + 512);
-        const int et = sw * 32 + lane;
-        if (et < 128) {
-            const int nn = tn * 128 + et;
-            const int neuron = ids[nn < cnt ? nn : cnt - 1];
-            s_ids[et] = neuron;
-            s_b1[et] = p.b1[neuron];
-        }
-        named_bar_sync(1, 128 * NT);
-        mbar_wait(done, 0);
+        const int ept = threadIdx.x - 128;
+        const uint32_t row_bytes = (uint32_t)p.chunk * 2u;
+        const int pieces = (int)(row_bytes / 16u);
+        const uint32_t dp = (uint32_t)TN * 2u + 16u;
+        uint8_t* stg_act = smem;
+        uint8_t* stg_dl = smem + (((uint32_t)TN * row_bytes + 1023u) & ~1023u);
+        mbar_wait(done, 0);  // all MMAs done: the ring is free
         tc_fence_after();
-        const uint32_t tacc = tmem + ((uint32_t)(quad * 32) << 16) + t * 128;
-        __nv_bfloat16* drow = p.delta + ((int64_t)z * p.chunk + r) * p.k_pad + tn * 128;
-        __nv_bfloat16* __restrict__ cache_base = p.act_cm + (int64_t)z * p.f * p.chunk + r;
+        if (sw == 0 && lane == 0) MLP_TRACE(128);
+        {
+            const char* cache_z = reinterpret_cast<const char*>(p.act_cm + (int64_t)z * p.f * p.chunk);
+            for (int idx = ept; idx < nval * pieces; idx += 128 * NT) {
+                const int n = idx / pieces, pc = idx - n * pieces;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(stg_act + n * row_bytes + pc * 16)),
+                             "l"(cache_z + (int64_t)s_ids[n] * row_bytes + pc * 16) : "memory");
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+        }
+        named_bar_sync(1, 128 * NT);  // the whole act tile has landed
+        if (sw == 0 && lane == 0) MLP_TRACE(130);
+        const uint32_t tacc = tmem + ((uint32_t)(quad * 32) << 16) + t * kUpMaxTN;
 #pragma unroll 1
-        for (int cc = 0; cc < 4; ++cc) {
-            uint32_t acc[32];
-            tmem_ld32(tacc + cc * 32, acc);
+        for (int g = 0; g < TN / 16; ++g) {
+            uint32_t acc[16];
+            tmem_ld16(tacc + g * 16, acc);
             tmem_ld_wait();
             if (!row_ok) continue;
-            const int nvalid = min(32, cnt - (tn * 128 + cc * 32));
-            float old[32], dl[32];
+            uint32_t pk[8];
+            __nv_bfloat16* ap0 = reinterpret_cast<__nv_bfloat16*>(stg_act + g * 16 * row_bytes) + r;
+            const int nv = nval - g * 16;  // live neurons in this group (uniform)
+            if (nv >= 16) {  // branch-free: the 16 chains interleave
+                float an[16], ol[16];
 #pragma unroll
-            for (int i = 0; i < 32; ++i)  // all loads first (independent)
-                old[i] = i < nvalid ? __bfloat162float(cache_base[(int64_t)s_ids[cc * 32 + i] * p.chunk])
-                                    : 0.f;
+                for (int i = 0; i < 16; ++i) ol[i] = __bfloat162float(ap0[i * (row_bytes / 2)]);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                dl[i] = 0.f;
-                if (i < nvalid) {
-                    const float a = fast_gelu(__uint_as_float(acc[i]) + s_b1[cc * 32 + i]);
-                    const __nv_bfloat16 a16 = __float2bfloat16_rn(a);
-                    cache_base[(int64_t)s_ids[cc * 32 + i] * p.chunk] = a16;
-                    dl[i] = __bfloat162float(a16) - old[i];
+                for (int i = 0; i < 16; ++i)
+                    an[i] = __bfloat162float(__float2bfloat16_rn(
+                        gelu_tanh_approx(__uint_as_float(acc[i]) + s_b1[g * 16 + i])));
+#pragma unroll
+                for (int i = 0; i < 16; ++i) ap0[i * (row_bytes / 2)] = __float2bfloat16_rn(an[i]);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    pk[i] = pack_bf16x2(an[2 * i] - ol[2 * i], an[2 * i + 1] - ol[2 * i + 1]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) {
+                    float d2[2];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        __nv_bfloat16* ap = ap0 + (i + u) * (row_bytes / 2);
+                        const float a = gelu_tanh_approx(__uint_as_float(acc[i + u]) + s_b1[g * 16 + i + u]);
+                        const __nv_bfloat16 a16 = __float2bfloat16_rn(a);
+                        d2[u] = 0.f;
+                        if (i + u < nv) {
+                            d2[u] = __bfloat162float(a16) - __bfloat162float(*ap);
+                            *ap = a16;
+                        }
+                    }
+                    pk[i / 2] = pack_bf16x2(d2[0], d2[1]);
                 }
             }
-            uint4* dst = reinterpret_cast<uint4*>(drow + cc * 32);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                uint4 v;
-                v.x = pack_bf16x2(dl[q * 8 + 0], dl[q * 8 + 1]);
-                v.y = pack_bf16x2(dl[q * 8 + 2], dl[q * 8 + 3]);
-                v.z = pack_bf16x2(dl[q * 8 + 4], dl[q * 8 + 5]);
-                v.w = pack_bf16x2(dl[q * 8 + 6], dl[q * 8 + 7]);
-                dst[q] = v;
+            uint4* dd = reinterpret_cast<uint4*>(stg_dl + r * dp + g * 32);
+            dd[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            dd[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+        named_bar_sync(1, 128 * NT);
+        if (sw == 0 && lane == 0) MLP_TRACE(131);
+        {   // act tile out and delta tile out: coalesced 16-byte stores
+            char* cache_z = reinterpret_cast<char*>(p.act_cm + (int64_t)z * p.f * p.chunk);
+            for (int idx = ept; idx < nval * pieces; idx += 128 * NT) {
+                const int n = idx / pieces, pc = idx - n * pieces;
+                *reinterpret_cast<uint4*>(cache_z + (int64_t)s_ids[n] * row_bytes + pc * 16) =
+                    *reinterpret_cast<const uint4*>(stg_act + n * row_bytes + pc * 16);
+            }
+            const int dpc = TN / 8;  // 16-byte pieces per delta row of this tile
+            for (int idx = ept; idx < p.chunk * dpc; idx += 128 * NT) {
+                const int rr = idx / dpc, pc = idx - rr * dpc;
+                *reinterpret_cast<uint4*>(drow0 + (int64_t)rr * p.k_pad + n0 + pc * 8) =
+                    *reinterpret_cast<const uint4*>(stg_dl + rr * dp + pc * 16);
+            }
+            // the last tile also zeroes the padding columns [n0 + TN, k_pad) the down GEMM reads
+            if (n0 + TN < p.k_pad && (tn + 1) * TN >= cnt) {
+                const int zc = (p.k_pad - n0 - TN) / 8;
+                for (int idx = ept; idx < p.chunk * zc; idx += 128 * NT) {
+                    const int rr = idx / zc, pc = idx - rr * zc;
+                    *reinterpret_cast<uint4*>(drow0 + (int64_t)rr * p.k_pad + n0 + TN + pc * 8) =
+                        make_uint4(0, 0, 0, 0);
+                }
             }
         }
     }
+    if (threadIdx.x == 128) MLP_TRACE(129);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -236,7 +376,7 @@ k_smlp_up(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUte
 
 // ------------------------------------------------------------------ down projection
 template <int NT>
-__global__ void __launch_bounds__(MlpLayout<NT>::kThreads, 2)
+__global__ void __launch_bounds__(MlpLayout<NT>::kThreads, 1)
 k_smlp_down(const __grid_constant__ CUtensorMap tm_delta,
             const __grid_constant__ CUtensorMap tm_w2g, const MlpParams p) {
     using L = MlpLayout<NT>;
@@ -267,44 +407,71 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta,
 
     uint64_t *full, *empty, *done;
     uint32_t tmem;
-    mlp_setup<NT>(smem, full, empty, done, tmem);
+    if (threadIdx.x == 0) MLP_TRACE(200);
+    mlp_setup<NT>(smem, full, empty, done, tmem, 1 + (L::kThreads - 32));
+    if (threadIdx.x == 0) MLP_TRACE(201);
 
-    if (warp == 0 || warp == 2 || warp == 3) {
-        const int pw = warp == 0 ? 0 : warp - 1;
-        const bool mine = (lane % 3) == pw;
-        if (warp == 0 && lane == 0) {
-            tma_prefetch_desc(&tm_delta);
-            tma_prefetch_desc(&tm_w2g);
+    if (warp != 1) {
+        // Producers = every warp but the MMA warp.  Warp 0 lane 0: delta tiles by TMA.  The
+        // B tile (64 gathered W2 rows x 128 D columns, MN-major: two 64-column strips of
+        // 64 x 128 B) is staged with cp.async, one row's 16 pieces on consecutive threads;
+        // the next k-block's neuron ids are loaded while this one's copies are issued.
+        const int ct = threadIdx.x < 32 ? threadIdx.x : threadIdx.x - 32;
+        constexpr int kCopyThreads = L::kThreads - 32;
+        constexpr int kPer = (64 * 16 + kCopyThreads - 1) / kCopyThreads;
+        int rowi[kPer];
+        uint32_t dso[kPer];
+        int coff[kPer];
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const int idx = ct + i * kCopyThreads;
+            const int row = idx >> 4, piece = idx & 15;
+            rowi[i] = idx < 64 * 16 ? row : -1;
+            dso[i] = (uint32_t)((piece >> 3) * 8192 + (row & 63) * 128 + (((piece & 7) ^ (row & 7)) << 4));
+            coff[i] = td * 128 + piece * 8;
         }
-        const int strip = lane >> 4, g4 = lane & 15;  // 16 lanes x 4 rows per 64-column strip
+        auto load_ids = [&](int kb, int (&nid)[kPer]) {
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                int nn = kb * 64 + (rowi[i] < 0 ? 0 : rowi[i]);
+                nid[i] = __ldg(ids + (nn < cnt ? nn : cnt - 1));  // pad: a valid row (delta = 0)
+            }
+        };
+        int nid_n[kPer];
+        load_ids(0, nid_n);
+        if (warp == 0 && lane == 0) tma_prefetch_desc(&tm_delta);
+        const uint32_t sB0 = smem_u32(smem + L::kB);
         for (int kb = 0; kb < kblocks; ++kb) {
             const int s = kb % kMlpStages;
-            int32_t rows[4];
+            int nid[kPer];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                int nn = kb * 64 + g4 * 4 + i;
-                rows[i] = ids[nn < cnt ? nn : cnt - 1];
-            }
+            for (int i = 0; i < kPer; ++i) nid[i] = nid_n[i];
+            if (kb + 1 < kblocks) load_ids(kb + 1, nid_n);
             if (kb >= kMlpStages) mbar_wait(empty + s, ((kb / kMlpStages) - 1) & 1);
             if (warp == 0 && lane == 0) {
-                mbar_arrive_expect_tx(full + s, (NT + 1) * kTile);
+                mbar_arrive_expect_tx(full + s, NT * kTile);
                 for (int t = 0; t < NT; ++t)
                     tma_load_2d(&tm_delta, full + s, smem + L::kA + (s * NT + t) * kTile, kb * 64,
                                 z * p.chunk + t * 128);
             }
-            // B tile: 64 neuron rows x 128 D columns as two 64-column (128 B) strips of 8 KB
-            if (mine)
-                tma_gather4(&tm_w2g, full + s, smem + L::kB + s * kTile + strip * 8192 + g4 * 512,
-                            td * 128 + strip * 64, rows[0], rows[1], rows[2], rows[3]);
+#pragma unroll
+            for (int i = 0; i < kPer; ++i)
+                if (rowi[i] >= 0)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sB0 + s * kTile + dso[i]),
+                                 "l"(p.w2 + (int64_t)nid[i] * p.d + coff[i]) : "memory");
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)) : "memory");
         }
-    } else if (warp == 1) {
+    }
+    if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t id = idesc_bf16(128, 128, false, true);
             const uint32_t sA = smem_u32(smem + L::kA), sB = smem_u32(smem + L::kB);
             for (int kb = 0; kb < kblocks; ++kb) {
                 const int s = kb % kMlpStages;
                 mbar_wait(full + s, (kb / kMlpStages) & 1);
+                fence_proxy_async_smem();  // cp.async (generic proxy) data -> tcgen05 reads
                 tc_fence_after();
+                MLP_TRACE(202 + kb);
                 for (int t = 0; t < NT; ++t) {
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)
@@ -322,6 +489,7 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta,
         const bool row_ok = r < p.chunk;
         mbar_wait(done, 0);
         tc_fence_after();
+        if (sw == 0 && lane == 0) MLP_TRACE(230);
         const uint32_t tacc = tmem + ((uint32_t)(quad * 32) << 16) + t * 128;
         float* orow = p.out_cache + ((int64_t)b * p.n + (int64_t)c * p.chunk + r) * p.d + td * 128;
 #pragma unroll 1
@@ -349,6 +517,7 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta,
                 residual32(p, (int64_t)b * p.n + (int64_t)c * p.chunk + r, td * 128 + cc * 32, m);
         }
     }
+    if (threadIdx.x == 128) MLP_TRACE(231);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -358,8 +527,11 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta,
 }
 
 bool mlp_tc_supported(int64_t d, int64_t chunk) {
-    return d % 128 == 0 && chunk >= 1 && chunk <= 256;
+    // chunk % 8: a neuron's chunk-major cache row (chunk x 2 B) moves by 16-byte bulk copies
+    return d % 128 == 0 && chunk >= 8 && chunk <= 256 && chunk % 8 == 0;
 }
+
+void smlp_geometry(int64_t k_max, int64_t nz, int* tn_width, int* ntiles, int64_t* k_pad);
 
 template <int NT>
 static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, const void* w2,
@@ -368,17 +540,23 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
                                void* act_cm, float* out_cache, void* delta_ws, int64_t k_pad,
                                cudaStream_t s, const void* x_mid, void* x_out) {
     using L = MlpLayout<NT>;
+    using LU = UpLayout<NT>;
     const int64_t nc = n / chunk;
-    CUtensorMap tx, tw1, tdl, tw2;
-    if (!make_map_bf16(&tx, x, d, batch * n, d, 128) || !make_map_bf16(&tw1, w1, d, f, d, 1) ||
+    int tn_width = 0, ntiles = 0;
+    smlp_geometry(k_max, batch * nc, &tn_width, &ntiles, nullptr);
+    CUtensorMap tx, tdl, tw2;
+    if (!make_map_bf16(&tx, x, d, batch * n, d, 128) ||
         !make_map_bf16(&tdl, delta_ws, k_pad, batch * nc * chunk, k_pad, 128) ||
         !make_map_bf16(&tw2, w2, d, f, d, 1))
         return cudaErrorInvalidValue;
     MlpParams p{};
+    p.w1 = (const __nv_bfloat16*)w1;
+    p.w2 = (const __nv_bfloat16*)w2;
     p.idx = idx;
     p.counts = counts;
     p.k_max = (int)k_max;
     p.k_pad = (int)k_pad;
+    p.tn_width = tn_width;
     p.b1 = b1;
     p.act_cm = (__nv_bfloat16*)act_cm;
     p.delta = (__nv_bfloat16*)delta_ws;
@@ -392,12 +570,12 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
     p.d = (int)d;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_smlp_up<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
+        cudaFuncSetAttribute(k_smlp_up<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, LU::kMaxSmem);
         cudaFuncSetAttribute(k_smlp_down<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
         attr = true;
     }
-    dim3 g1((unsigned)((k_max + 127) / 128), (unsigned)(batch * nc));
-    k_smlp_up<NT><<<g1, L::kThreads, L::kSmemAlloc, s>>>(tx, tw1, p);
+    dim3 g1((unsigned)ntiles, (unsigned)(batch * nc));
+    k_smlp_up<NT><<<g1, LU::kThreads, LU::alloc(tn_width), s>>>(tx, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 g2((unsigned)(d / 128), (unsigned)(batch * nc));
@@ -405,7 +583,35 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
     return cudaGetLastError();
 }
 
-// delta workspace: [B*C*chunk rows][k_pad] bf16, k_pad = round_up(k_max, 128)
+// Up-projection tiling: as many neuron tiles per chunk as fit ONE wave over the SMs
+// (FLUX: 24 chunks -> 6 tiles of 144 for k = 860), width a multiple of 16 in [64, 192].
+// The delta workspace is [B*C*chunk rows][k_pad] bf16, k_pad = round_up(tiles * width, 64)
+// (the down GEMM's 64-neuron k-blocks read up to round_up(count, 64) columns).
+void smlp_geometry(int64_t k_max, int64_t nz, int* tn_width, int* ntiles, int64_t* k_pad) {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const int64_t km = std::max<int64_t>(k_max, 1);
+    const int64_t fit = std::max<int64_t>(1, sms / std::max<int64_t>(nz, 1));
+    int64_t w = (km + fit - 1) / fit;
+    w = (w + 15) / 16 * 16;
+    w = std::min<int64_t>(std::max<int64_t>(w, 64), kUpMaxTN);
+    const int64_t t = (km + w - 1) / w;
+    if (tn_width) *tn_width = (int)w;
+    if (ntiles) *ntiles = (int)t;
+    if (k_pad) *k_pad = (t * w + 63) / 64 * 64;
+}
+
+int64_t prod_smlp_delta_cols(int64_t k_max, int64_t nz) {
+    int64_t k_pad = 0;
+    smlp_geometry(k_max, nz, nullptr, nullptr, &k_pad);
+    return k_pad;
+}
+
 cudaError_t prod_sparse_delta_mlp_tc(const void* x, const void* w1, const float* b1,
                                      const void* w2, const int32_t* idx, const int32_t* counts,
                                      int64_t k_max, int64_t chunk, int64_t batch, int64_t n,
@@ -414,7 +620,8 @@ cudaError_t prod_sparse_delta_mlp_tc(const void* x, const void* w1, const float*
                                      void* x_out) {
     if (!mlp_tc_supported(d, chunk)) return cudaErrorNotSupported;
     if (k_max == 0) return cudaSuccess;
-    const int64_t k_pad = (k_max + 127) / 128 * 128;
+    int64_t k_pad = 0;
+    smlp_geometry(k_max, batch * (n / chunk), nullptr, nullptr, &k_pad);
     if (chunk > 128)
         return launch_smlp<2>(x, w1, b1, w2, idx, counts, k_max, chunk, batch, n, d, f, act_cm,
                               out_cache, delta_ws, k_pad, s, x_mid, x_out);
@@ -424,3 +631,9 @@ cudaError_t prod_sparse_delta_mlp_tc(const void* x, const void* w1, const float*
 
 }  // namespace dev
 }  // namespace csd
+
+// Debug only (scripts/mlp_trace.py): timeline buffer of 8 x 256 uint64 for k_smlp_up.
+extern "C" int csd_debug_set_mlp_trace(void* dev_buf) {
+    uint64_t* p = static_cast<uint64_t*>(dev_buf);
+    return cudaMemcpyToSymbol(csd::dev::g_mlp_trace, &p, sizeof(p)) == cudaSuccess ? 0 : 7;
+}
