@@ -61,6 +61,7 @@ struct MlpParams {
     const int32_t* counts;
     int k_max, k_pad;
     int tn_width;  // neurons per up-projection tile (multiple of 16, <= kUpMaxTN)
+    int nz;        // chunks (batch x C)
     const float* b1;
     __nv_bfloat16* act_cm;
     __nv_bfloat16* delta;
@@ -375,149 +376,215 @@ k_smlp_up(const __grid_constant__ CUtensorMap tm_x, const MlpParams p) {
 }
 
 // ------------------------------------------------------------------ down projection
+// Persistent: item = (chunk z, 128-column D tile td), items strided over min(items, SMs)
+// CTAs.  Per item: M_cache[z rows, td cols] += delta[z rows, :cnt] W2[S][:, td cols]
+// (M = chunk rows as NT x 128, N = 128, K = cnt in 64-neuron k-blocks), then the residual
+// x_out = x_mid + M_cache (north_star item 5: the cache update fused into the epilogue).
+// The TMEM accumulator is double-buffered so an item's epilogue overlaps the next item's
+// K loop.  Stage = delta tile (TMA) + 64 gathered W2 rows x 128 columns (cp.async, MN-major).
+constexpr int kDnStages = 3;
 template <int NT>
-__global__ void __launch_bounds__(MlpLayout<NT>::kThreads, 1)
-k_smlp_down(const __grid_constant__ CUtensorMap tm_delta,
-            const __grid_constant__ CUtensorMap tm_w2g, const MlpParams p) {
-    using L = MlpLayout<NT>;
+struct DnLayout {
+    static constexpr uint32_t kStage = NT * kTile + kTile;  // A (rows x 64 k) + B (64 k x 128)
+    static constexpr uint32_t kStg = kStage * kDnStages;    // epilogue transposition buffers
+    static constexpr uint32_t kStgBytes = 4 * NT * 4096;     // one 32 x 32 fp32 block per warp
+    static constexpr uint32_t kBar = kStg + kStgBytes;
+    static constexpr uint32_t kAlloc = kBar + 256 + 1024;
+    static constexpr uint32_t kThreads = 128 + 128 * NT;
+    static constexpr uint32_t kTmemCols = 2 * NT * 128 <= 256 ? 256 : 512;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(DnLayout<NT>::kThreads, 1)
+k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
+    using L = DnLayout<NT>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int z = blockIdx.y, td = blockIdx.x;
-    const int cnt = p.counts[z];
-    const int b = z / p.chunks, c = z % p.chunks;
-    if (cnt == 0) {  // no recomputed neurons: M_cache unchanged, only the residual
-        if (p.x_out != nullptr) {
-            for (int r = threadIdx.x; r < p.chunk; r += blockDim.x) {
-                const int64_t row = (int64_t)b * p.n + (int64_t)c * p.chunk + r;
-                for (int cc = 0; cc < 4; ++cc) {
-                    float m[32];
-                    const float* src = p.out_cache + row * p.d + td * 128 + cc * 32;
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) m[i] = src[i];
-                    residual32(p, row, td * 128 + cc * 32, m);
-                }
-            }
+    const int ntd = p.d / 128;
+    const int items = p.nz * ntd;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
+    uint64_t* full = bars;                    // [kDnStages]
+    uint64_t* empty = bars + kDnStages;       // [kDnStages]
+    uint64_t* tfull = bars + 2 * kDnStages;   // [2] accumulator buffer final
+    uint64_t* tempty = tfull + 2;             // [2] accumulator buffer drained
+    uint32_t* slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    constexpr int kCopyThreads = 96;          // warps 0, 2, 3
+    if (threadIdx.x == 0) {
+        if (blockIdx.x == 0) MLP_TRACE(200);
+        for (int s = 0; s < kDnStages; ++s) {
+            mbar_init(full + s, 1 + kCopyThreads);
+            mbar_init(empty + s, 1);
         }
-        return;
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(tfull + i, 1);
+            mbar_init(tempty + i, 128 * NT);
+        }
+        fence_barrier_init();
     }
-    const int kblocks = (cnt + 63) / 64;
-    const int32_t* ids = p.idx + (int64_t)z * p.k_max;
+    if (warp == 1) tmem_alloc<L::kTmemCols>(slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *slot;
+    auto kblocks_of = [&](int item) { return (p.counts[item / ntd] + 63) / 64; };
 
-    uint64_t *full, *empty, *done;
-    uint32_t tmem;
-    if (threadIdx.x == 0) MLP_TRACE(200);
-    mlp_setup<NT>(smem, full, empty, done, tmem, 1 + (L::kThreads - 32));
-    if (threadIdx.x == 0) MLP_TRACE(201);
-
-    if (warp != 1) {
-        // Producers = every warp but the MMA warp.  Warp 0 lane 0: delta tiles by TMA.  The
-        // B tile (64 gathered W2 rows x 128 D columns, MN-major: two 64-column strips of
-        // 64 x 128 B) is staged with cp.async, one row's 16 pieces on consecutive threads;
-        // the next k-block's neuron ids are loaded while this one's copies are issued.
-        const int ct = threadIdx.x < 32 ? threadIdx.x : threadIdx.x - 32;
-        constexpr int kCopyThreads = L::kThreads - 32;
+    if (warp == 0 || warp == 2 || warp == 3) {
+        // producers: warp 0 lane 0 the delta tiles (TMA); all 96 threads the W2 k-slices,
+        // one row's 16 pieces (2 strips x 8) on consecutive threads
+        const int ct = warp == 0 ? lane : (warp - 1) * 32 + lane;
         constexpr int kPer = (64 * 16 + kCopyThreads - 1) / kCopyThreads;
-        int rowi[kPer];
-        uint32_t dso[kPer];
-        int coff[kPer];
-#pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-            const int idx = ct + i * kCopyThreads;
-            const int row = idx >> 4, piece = idx & 15;
-            rowi[i] = idx < 64 * 16 ? row : -1;
-            dso[i] = (uint32_t)((piece >> 3) * 8192 + (row & 63) * 128 + (((piece & 7) ^ (row & 7)) << 4));
-            coff[i] = td * 128 + piece * 8;
-        }
-        auto load_ids = [&](int kb, int (&nid)[kPer]) {
-#pragma unroll
-            for (int i = 0; i < kPer; ++i) {
-                int nn = kb * 64 + (rowi[i] < 0 ? 0 : rowi[i]);
-                nid[i] = __ldg(ids + (nn < cnt ? nn : cnt - 1));  // pad: a valid row (delta = 0)
-            }
-        };
-        int nid_n[kPer];
-        load_ids(0, nid_n);
         if (warp == 0 && lane == 0) tma_prefetch_desc(&tm_delta);
-        const uint32_t sB0 = smem_u32(smem + L::kB);
-        for (int kb = 0; kb < kblocks; ++kb) {
-            const int s = kb % kMlpStages;
-            int nid[kPer];
+        const uint32_t s0 = smem_u32(smem);
+        uint32_t gk = 0;  // global k-block counter (ring position)
+        for (int item = blockIdx.x; item < items; item += gridDim.x) {
+            const int z = item / ntd, td = item - z * ntd;
+            const int cnt = p.counts[z];
+            const int kbs = (cnt + 63) / 64;
+            const int32_t* ids = p.idx + (int64_t)z * p.k_max;
+            for (int kb = 0; kb < kbs; ++kb, ++gk) {
+                const int s = gk % kDnStages;
+                int nid[kPer];
 #pragma unroll
-            for (int i = 0; i < kPer; ++i) nid[i] = nid_n[i];
-            if (kb + 1 < kblocks) load_ids(kb + 1, nid_n);
-            if (kb >= kMlpStages) mbar_wait(empty + s, ((kb / kMlpStages) - 1) & 1);
-            if (warp == 0 && lane == 0) {
-                mbar_arrive_expect_tx(full + s, NT * kTile);
-                for (int t = 0; t < NT; ++t)
-                    tma_load_2d(&tm_delta, full + s, smem + L::kA + (s * NT + t) * kTile, kb * 64,
-                                z * p.chunk + t * 128);
+                for (int i = 0; i < kPer; ++i) {
+                    const int idx = ct + i * kCopyThreads;
+                    int nn = kb * 64 + ((idx >> 4) & 63);
+                    nid[i] = __ldg(ids + (nn < cnt ? nn : cnt - 1));  // pad: a valid row (delta = 0)
+                }
+                if (gk >= kDnStages) mbar_wait(empty + s, ((gk / kDnStages) - 1) & 1);
+                if (warp == 0 && lane == 0) {
+                    mbar_arrive_expect_tx(full + s, NT * kTile);
+                    for (int t = 0; t < NT; ++t)
+                        tma_load_2d(&tm_delta, full + s, smem + s * L::kStage + t * kTile, kb * 64,
+                                    z * p.chunk + t * 128);
+                }
+#pragma unroll
+                for (int i = 0; i < kPer; ++i) {
+                    const int idx = ct + i * kCopyThreads;
+                    if (idx < 64 * 16) {
+                        const int row = idx >> 4, piece = idx & 15;
+                        const uint32_t d = s0 + s * L::kStage + NT * kTile + (piece >> 3) * 8192 + row * 128 +
+                                           (((piece & 7) ^ (row & 7)) << 4);
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d),
+                                     "l"(p.w2 + (int64_t)nid[i] * p.d + td * 128 + piece * 8) : "memory");
+                    }
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)) : "memory");
             }
-#pragma unroll
-            for (int i = 0; i < kPer; ++i)
-                if (rowi[i] >= 0)
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sB0 + s * kTile + dso[i]),
-                                 "l"(p.w2 + (int64_t)nid[i] * p.d + coff[i]) : "memory");
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)) : "memory");
         }
-    }
-    if (warp == 1) {
+    } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t id = idesc_bf16(128, 128, false, true);
-            const uint32_t sA = smem_u32(smem + L::kA), sB = smem_u32(smem + L::kB);
-            for (int kb = 0; kb < kblocks; ++kb) {
-                const int s = kb % kMlpStages;
-                mbar_wait(full + s, (kb / kMlpStages) & 1);
-                fence_proxy_async_smem();  // cp.async (generic proxy) data -> tcgen05 reads
+            const uint32_t s0 = smem_u32(smem);
+            uint32_t gk = 0, li = 0;
+            for (int item = blockIdx.x; item < items; item += gridDim.x, ++li) {
+                const int kbs = kblocks_of(item);
+                const uint32_t ab = li & 1;
+                if (li >= 2) mbar_wait(tempty + ab, ((li >> 1) - 1) & 1);  // buffer drained
                 tc_fence_after();
-                MLP_TRACE(202 + kb);
-                for (int t = 0; t < NT; ++t) {
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        mma_bf16(tmem + t * 128, desc_kmajor_sw128(sA + (s * NT + t) * kTile + kk * 32),
-                                 desc_mnmajor_sw128(sB + s * kTile + kk * 2048, 8192), id,
-                                 (kb > 0 || kk > 0) ? 1u : 0u);
+                const uint32_t acc = tmem + ab * (NT * 128);
+                if (kbs == 0) {  // nothing to accumulate: the epilogue adds zero
+                    mma_commit(tfull + ab);
+                    continue;
                 }
-                mma_commit(empty + s);
+                for (int kb = 0; kb < kbs; ++kb, ++gk) {
+                    const int s = gk % kDnStages;
+                    mbar_wait(full + s, (gk / kDnStages) & 1);
+                    fence_proxy_async_smem();  // cp.async (generic proxy) data -> tcgen05 reads
+                    tc_fence_after();
+                    if (blockIdx.x == 0 && li == 0) MLP_TRACE(202 + kb);
+                    const uint32_t sa = s0 + s * L::kStage, sb = sa + NT * kTile;
+                    for (int t = 0; t < NT; ++t) {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            mma_bf16(acc + t * 128, desc_kmajor_sw128(sa + t * kTile + kk * 32),
+                                     desc_mnmajor_sw128(sb + kk * 2048, 8192), id,
+                                     (kb > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    mma_commit(empty + s);
+                }
+                mma_commit(tfull + ab);
             }
-            mma_commit(done);
         }
-    } else if (warp >= 4) {
+    } else {
+        // epilogue warps: thread = chunk row for the TMEM read; each warp then transposes
+        // 32 x 32 fp32 blocks through its own smem slice so the M_cache read-modify-write and
+        // the residual run row-contiguously (8 lanes x 16 B per 32-column row segment)
         const int sw = warp - 4, t = sw >> 2, quad = warp & 3;
         const int r = t * 128 + quad * 32 + lane;
-        const bool row_ok = r < p.chunk;
-        mbar_wait(done, 0);
-        tc_fence_after();
-        if (sw == 0 && lane == 0) MLP_TRACE(230);
-        const uint32_t tacc = tmem + ((uint32_t)(quad * 32) << 16) + t * 128;
-        float* orow = p.out_cache + ((int64_t)b * p.n + (int64_t)c * p.chunk + r) * p.d + td * 128;
-#pragma unroll 1
-        for (int cc = 0; cc < 4; ++cc) {
-            uint32_t acc[32];
-            tmem_ld32(tacc + cc * 32, acc);
-            tmem_ld_wait();
-            if (!row_ok) continue;
-            float4* o4 = reinterpret_cast<float4*>(orow + cc * 32);
-            float m[32];
-            float4 v[8];
+        float* stg = reinterpret_cast<float*>(smem + L::kStg + sw * 4096);
+        const bool warp_live = t * 128 + quad * 32 < p.chunk;
+        uint32_t li = 0;
+        for (int item = blockIdx.x; item < items; item += gridDim.x, ++li) {
+            const int z = item / ntd, td = item - z * ntd;
+            const bool has_acc = p.counts[z] > 0;
+            const uint32_t ab = li & 1;
+            mbar_wait(tfull + ab, (li >> 1) & 1);
+            tc_fence_after();
+            if (blockIdx.x == 0 && sw == 0 && lane == 0 && li == 0) MLP_TRACE(230);
+            const uint32_t tacc = tmem + ab * (NT * 128) + ((uint32_t)(quad * 32) << 16) + t * 128;
+            const int b = z / p.chunks, c = z - b * p.chunks;
+            const int64_t row0 = (int64_t)b * p.n + (int64_t)c * p.chunk + t * 128 + quad * 32;
+            for (int oc = 0; oc < 4; ++oc) {
+                uint32_t v[32];
+                if (has_acc) {
+                    tmem_ld32(tacc + oc * 32, v);
+                    tmem_ld_wait();
+                } else {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) v[q] = o4[q];  // batch the loads
+                    for (int i = 0; i < 32; ++i) v[i] = 0u;
+                }
+                if (oc == 3) {  // TMEM reads of this buffer done: let the next-but-one item in
+                    tc_fence_before();
+                    mbar_arrive(tempty + ab);
+                }
+                if (!warp_live) continue;
+                __syncwarp();
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                v[q].x += __uint_as_float(acc[q * 4 + 0]);
-                v[q].y += __uint_as_float(acc[q * 4 + 1]);
-                v[q].z += __uint_as_float(acc[q * 4 + 2]);
-                v[q].w += __uint_as_float(acc[q * 4 + 3]);
-                m[q * 4 + 0] = v[q].x; m[q * 4 + 1] = v[q].y; m[q * 4 + 2] = v[q].z; m[q * 4 + 3] = v[q].w;
+                for (int q = 0; q < 8; ++q)
+                    *reinterpret_cast<uint4*>(stg + lane * 32 + ((q ^ (lane & 7)) << 2)) =
+                        make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                __syncwarp();
+                // lane -> (row rr = it * 4 + lane / 8, columns 4 (lane % 8) .. + 3); all the
+                // round's global loads are issued before any use (8 rows in flight per lane)
+                const int c4 = lane & 7;
+                const int col = td * 128 + oc * 32 + c4 * 4;
+                const int rlim = p.chunk - (t * 128 + quad * 32);  // live rows of this warp
+                float4 m[8];
+                uint2 xm[8];
+#pragma unroll
+                for (int it = 0; it < 8; ++it) {
+                    const int rr = it * 4 + (lane >> 3);
+                    if (rr < rlim) {
+                        const int64_t go = (row0 + rr) * p.d + col;
+                        m[it] = *reinterpret_cast<const float4*>(p.out_cache + go);
+                        if (p.x_out != nullptr) xm[it] = *reinterpret_cast<const uint2*>(p.x_mid + go);
+                    }
+                }
+#pragma unroll
+                for (int it = 0; it < 8; ++it) {
+                    const int rr = it * 4 + (lane >> 3);
+                    if (rr >= rlim) continue;
+                    const float4 a = *reinterpret_cast<const float4*>(stg + rr * 32 + ((c4 ^ (rr & 7)) << 2));
+                    const int64_t go = (row0 + rr) * p.d + col;
+                    float4 mm = m[it];
+                    mm.x += a.x;
+                    mm.y += a.y;
+                    mm.z += a.z;
+                    mm.w += a.w;
+                    *reinterpret_cast<float4*>(p.out_cache + go) = mm;
+                    if (p.x_out != nullptr) {
+                        const float2 x0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xm[it].x));
+                        const float2 x1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xm[it].y));
+                        *reinterpret_cast<uint2*>(p.x_out + go) =
+                            make_uint2(pack_bf16x2(x0.x + mm.x, x0.y + mm.y), pack_bf16x2(x1.x + mm.z, x1.y + mm.w));
+                    }
+                }
             }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) o4[q] = v[q];
-            if (p.x_out != nullptr)
-                residual32(p, (int64_t)b * p.n + (int64_t)c * p.chunk + r, td * 128 + cc * 32, m);
+            if (blockIdx.x == 0 && sw == 0 && lane == 0 && li == 0) MLP_TRACE(231);
         }
     }
-    if (threadIdx.x == 128) MLP_TRACE(231);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -544,10 +611,9 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
     const int64_t nc = n / chunk;
     int tn_width = 0, ntiles = 0;
     smlp_geometry(k_max, batch * nc, &tn_width, &ntiles, nullptr);
-    CUtensorMap tx, tdl, tw2;
+    CUtensorMap tx, tdl;
     if (!make_map_bf16(&tx, x, d, batch * n, d, 128) ||
-        !make_map_bf16(&tdl, delta_ws, k_pad, batch * nc * chunk, k_pad, 128) ||
-        !make_map_bf16(&tw2, w2, d, f, d, 1))
+        !make_map_bf16(&tdl, delta_ws, k_pad, batch * nc * chunk, k_pad, 128))
         return cudaErrorInvalidValue;
     MlpParams p{};
     p.w1 = (const __nv_bfloat16*)w1;
@@ -568,18 +634,26 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
     p.chunks = (int)nc;
     p.f = (int)f;
     p.d = (int)d;
+    p.nz = (int)(batch * nc);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_smlp_up<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, LU::kMaxSmem);
-        cudaFuncSetAttribute(k_smlp_down<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
+        cudaFuncSetAttribute(k_smlp_down<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, DnLayout<NT>::kAlloc);
         attr = true;
     }
     dim3 g1((unsigned)ntiles, (unsigned)(batch * nc));
     k_smlp_up<NT><<<g1, LU::kThreads, LU::alloc(tn_width), s>>>(tx, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    dim3 g2((unsigned)(d / 128), (unsigned)(batch * nc));
-    k_smlp_down<NT><<<g2, L::kThreads, L::kSmemAlloc, s>>>(tdl, tw2, p);
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t items = batch * nc * (d / 128);
+    k_smlp_down<NT><<<(unsigned)std::min<int64_t>(items, sms), DnLayout<NT>::kThreads,
+                      DnLayout<NT>::kAlloc, s>>>(tdl, p);
     return cudaGetLastError();
 }
 
