@@ -195,6 +195,13 @@ csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int den
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (!dense && (!blk->attn_init || !blk->mlp_init))
         return set_error(CSD_ERR_STATE, "sparse attention step requested before any dense step");
+    // PROD: the selected index sets feed order-invariant kernels -> skip the per-row sort
+    struct SortGuard {
+        Ctx* c;
+        bool old;
+        ~SortGuard() { c->sorted_topk = old; }
+    } sort_guard{blk->ctx, blk->ctx->sorted_topk};
+    blk->ctx->sorted_topk = md != CSD_MODE_PROD;
     const int64_t B = c.batch, N = c.seq, D = c.dim;
     const int64_t Dl = c.heads_local * c.head_dim, Fl = c.f_local;
     const int64_t mk = c.mlp_k > 0 ? c.mlp_k : Fl;

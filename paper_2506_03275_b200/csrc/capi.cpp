@@ -225,7 +225,7 @@ csd_status csd_select_top_k(csd_ctx* ctx, const float* scores, int64_t rows, int
                          (long long)m);
     if (rows < 1) return set_error(CSD_ERR_SHAPE, "select_top_k: no rows");
     if (k <= topk_max_k()) {
-        CSD_CU(topk_rows(scores, rows, m, k, idx, counts, S(stream)), "topk_rows");
+        CSD_CU(topk_rows(scores, rows, m, k, idx, counts, S(stream), c->sorted_topk), "topk_rows");
         c->launches += 1;
     } else {
         void* ws = c->ws(csd::kWsTopk, sizeof(uint64_t) * rows * k);

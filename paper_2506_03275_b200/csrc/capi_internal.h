@@ -37,6 +37,11 @@ struct Ctx {
     int64_t launches = 0;          // our kernels launched through this context
     int64_t library_launches = 0;  // cuBLAS GEMM calls
     bool validate_prod = true;     // PROD-mode async index validation
+    // select_top_k output order: descending score (the reference contract, sparse_index.cpp:
+    // 86-90).  The PROD block path clears it: its consumers (column-sparse attention,
+    // sparse-delta MLP) are order-invariant, so the same exact index SET in index order
+    // skips the per-row sort.
+    bool sorted_topk = true;
 
     void* ws(int slot, size_t bytes);
     cublasHandle_t blas();

@@ -52,7 +52,7 @@ cudaError_t check_sparse_delta_mlp(const float* x, const float* w1, const float*
 // ---- shared (both modes) ---------------------------------------------------
 // topk.cu
 cudaError_t topk_rows(const float* scores, int64_t rows, int64_t m, int64_t k, int32_t* idx,
-                      int32_t* counts, cudaStream_t s);
+                      int32_t* counts, cudaStream_t s, bool sorted = true);
 int64_t topk_max_k();
 cudaError_t topk_rows_global(const float* scores, int64_t rows, int64_t m, int64_t k,
                              int32_t* idx, int32_t* counts, uint64_t* ws, cudaStream_t s);

@@ -20,6 +20,14 @@
 namespace csd {
 namespace dev {
 
+// Debug timeline (scripts/topk_micro.py --trace): CTA 0 stamps clock64() per phase.
+__device__ uint64_t* g_topk_trace = nullptr;
+#define TOPK_TRACE(slot)                                                                  \
+    do {                                                                                  \
+        uint64_t* tr_ = g_topk_trace;                                                     \
+        if (tr_ != nullptr && blockIdx.x == 0 && threadIdx.x == 0) tr_[slot] = clock64();  \
+    } while (0)
+
 constexpr int kTopkThreads = 512;
 constexpr int kTopkWarps = kTopkThreads / 32;
 constexpr int64_t kTopkMaxSortK = 16384;         // 128 KB of u64 composites
@@ -31,39 +39,119 @@ __device__ __forceinline__ uint32_t ord_key(float x) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+// Bitonic sort (descending) of P = sort_pow2 64-bit keys in smem.  Strides >= 64 run over
+// smem with a block barrier per step; each run of strides 32..1 runs in registers: a warp
+// owns 64-element segments (element lane and 32 + lane), stride 32 is an in-thread swap and
+// strides 16..1 are shuffles.
+__device__ __forceinline__ void cmp_swap_desc(uint64_t& a, uint64_t& b, bool desc) {
+    if (desc ? (a < b) : (a > b)) {
+        const uint64_t t = a;
+        a = b;
+        b = t;
+    }
+}
+__device__ void bitonic_sort_desc(uint64_t* sel, int P) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int j = size >> 1; j >= 64; j >>= 1) {
+            for (int i = tid; i < P; i += kTopkThreads) {
+                const int q = i ^ j;
+                if (q > i) {
+                    uint64_t a = sel[i], b = sel[q];
+                    cmp_swap_desc(a, b, (i & size) == 0);
+                    sel[i] = a;
+                    sel[q] = b;
+                }
+            }
+            __syncthreads();
+        }
+        // strides min(size/2, 32) .. 1 in registers, one 64-element segment per warp pass
+        for (int seg = warp * 64; seg < P; seg += kTopkWarps * 64) {
+            uint64_t r0 = sel[seg + lane], r1 = sel[seg + 32 + lane];
+            const int i0 = seg + lane, i1 = seg + 32 + lane;
+            for (int j = min(size >> 1, 32); j >= 1; j >>= 1) {
+                if (j == 32) {
+                    cmp_swap_desc(r0, r1, (i0 & size) == 0);  // partners i0, i0 + 32
+                } else {
+                    // partner lane^j holds element i^j in the same register
+                    const bool lower = (lane & j) == 0;
+                    const uint64_t p0 = __shfl_xor_sync(0xffffffffu, r0, j);
+                    const uint64_t p1 = __shfl_xor_sync(0xffffffffu, r1, j);
+                    const bool d0 = (i0 & size) == 0, d1 = (i1 & size) == 0;
+                    // the lower index keeps the larger key when descending
+                    const bool take0 = lower ? (d0 ? p0 > r0 : p0 < r0) : (d0 ? p0 < r0 : p0 > r0);
+                    const bool take1 = lower ? (d1 ? p1 > r1 : p1 < r1) : (d1 ? p1 < r1 : p1 > r1);
+                    r0 = take0 ? p0 : r0;
+                    r1 = take1 ? p1 : r1;
+                }
+            }
+            sel[seg + lane] = r0;
+            sel[seg + 32 + lane] = r1;
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void __launch_bounds__(kTopkThreads)
 k_topk_rows(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* __restrict__ idx_out,
-            int32_t* __restrict__ counts, int stage_row, int sort_pow2) {
+            int32_t* __restrict__ counts, int stage_row, int sort_pow2, int sorted) {
     extern __shared__ __align__(16) uint8_t smem[];
-    uint64_t* sel = reinterpret_cast<uint64_t*>(smem);                 // [sort_pow2]
-    float* srow = reinterpret_cast<float*>(smem + sizeof(uint64_t) * sort_pow2);
+    uint64_t* sel = reinterpret_cast<uint64_t*>(smem);                         // [sort_pow2]
+    uint32_t* keys = reinterpret_cast<uint32_t*>(smem + sizeof(uint64_t) * sort_pow2);  // [m]
     __shared__ uint32_t hist[256];
-    __shared__ uint32_t warp_tot[kTopkWarps];
-    __shared__ uint32_t s_prefix, s_kleft, s_total, s_gt;
+    __shared__ uint32_t warp_tot[2][kTopkWarps];
+    __shared__ uint32_t warp_red[2][kTopkWarps];
+    __shared__ uint32_t s_prefix, s_kleft;
 
     const int64_t row = blockIdx.x;
     const float* src = scores + row * m;
-    const int tid = threadIdx.x;
-    if (stage_row) {
-        for (int64_t j = tid; j < m; j += kTopkThreads) srow[j] = src[j];
-        src = srow;
+    const int tid = threadIdx.x, lane = tid & 31, warp_id = tid >> 5;
+    TOPK_TRACE(0);
+    // ord keys (staged when the row fits) and their common leading bits (AND / OR reduce)
+    uint32_t kand = 0xffffffffu, kor = 0u;
+    for (int64_t j = tid; j < m; j += kTopkThreads) {
+        const uint32_t o = ord_key(src[j]);
+        if (stage_row) keys[j] = o;
+        kand &= o;
+        kor |= o;
     }
-    if (tid == 0) { s_prefix = 0; s_kleft = (uint32_t)k; s_gt = 0; }
+    kand = __reduce_and_sync(0xffffffffu, kand);
+    kor = __reduce_or_sync(0xffffffffu, kor);
+    if (lane == 0) {
+        warp_red[0][warp_id] = kand;
+        warp_red[1][warp_id] = kor;
+    }
     __syncthreads();
+    if (tid == 0) {
+        uint32_t a = 0xffffffffu, o = 0u;
+        for (int w = 0; w < kTopkWarps; ++w) {
+            a &= warp_red[0][w];
+            o |= warp_red[1][w];
+        }
+        const int lead = __clz(a ^ o);  // bits every key shares (32: all keys equal)
+        warp_red[0][0] = (uint32_t)lead;
+        s_prefix = lead >= 32 ? a : (a & ~(0xffffffffu >> lead));
+        s_kleft = (uint32_t)k;
+    }
+    __syncthreads();
+    const int lead = (int)warp_red[0][0];
+    TOPK_TRACE(1);
+    auto key_at = [&](int64_t j) -> uint32_t { return stage_row ? keys[j] : ord_key(src[j]); };
 
-    uint32_t mask = 0;
-    // per-warp private histograms: nearby scores share their top digits, so a single
-    // shared histogram serialises thousands of same-address atomics
+    // radix select over the differing bits only, 8 bits per pass from the top
     __shared__ uint32_t whist[kTopkWarps][256];
-    const int warp_id = tid >> 5;
-    for (int shift = 24; shift >= 0; shift -= 8) {
+    uint32_t mask = lead >= 32 ? 0xffffffffu : ~(0xffffffffu >> lead);
+    int pass = 0;
+    for (int top = 32 - lead; top > 0; top -= 8, ++pass) {
+        const int nb = min(8, top), shift = top - nb;
+        const uint32_t dmask = (1u << nb) - 1u;
         for (int i = tid; i < kTopkWarps * 256; i += kTopkThreads) (&whist[0][0])[i] = 0;
         __syncthreads();
         const uint32_t prefix = s_prefix;
         uint32_t* wh = whist[warp_id];
         for (int64_t j = tid; j < m; j += kTopkThreads) {
-            const uint32_t o = ord_key(src[j]);
-            if ((o & mask) == prefix) atomicAdd(&wh[(o >> shift) & 0xffu], 1u);
+            const uint32_t o = key_at(j);
+            if ((o & mask) == prefix) atomicAdd(&wh[(o >> shift) & dmask], 1u);
         }
         __syncthreads();
         for (int i = tid; i < 256; i += kTopkThreads) {
@@ -94,56 +182,70 @@ k_topk_rows(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* __r
                 run += c[i];
             }
         }
-        mask |= 0xffu << shift;
+        mask |= dmask << shift;
         __syncthreads();
+        TOPK_TRACE(2 + min(pass, 3));
     }
     const uint32_t T = s_prefix;
     const uint32_t need_eq = s_kleft;           // ties to take, lowest index first
     const uint32_t G = (uint32_t)k - need_eq;   // strictly greater
 
-    // collect: warp w owns the contiguous segment [w*seg, (w+1)*seg); one counting pass,
-    // one block scan of the per-warp tie counts (index order = warp order), one write pass
-    const int lane = tid & 31;
+    // collect, in index order: warp w owns the contiguous segment [w*seg, (w+1)*seg); one
+    // counting pass (ballots), one block scan of the per-warp counts, one write pass
     const int64_t seg = ((m + kTopkWarps * 32 - 1) / (kTopkWarps * 32)) * 32;
     const int64_t s0 = warp_id * seg, s1 = min(m, s0 + seg);
-    uint32_t n_eq = 0;
+    uint32_t n_gt = 0, n_eq = 0;
     for (int64_t j0 = s0; j0 < s1; j0 += 32) {
         const int64_t j = j0 + lane;
-        n_eq += __popc(__ballot_sync(0xffffffffu, j < s1 && ord_key(src[j]) == T));
+        const uint32_t o = j < s1 ? key_at(j) : 0u;
+        n_gt += __popc(__ballot_sync(0xffffffffu, j < s1 && o > T));
+        n_eq += __popc(__ballot_sync(0xffffffffu, j < s1 && o == T));
     }
-    if (lane == 0) warp_tot[warp_id] = n_eq;
+    if (lane == 0) {
+        warp_tot[0][warp_id] = n_gt;
+        warp_tot[1][warp_id] = n_eq;
+    }
     __syncthreads();
     if (tid < 32) {
-        const uint32_t v = tid < kTopkWarps ? warp_tot[tid] : 0u;
-        uint32_t incl = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (tid >= o) incl += t;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const uint32_t v = tid < kTopkWarps ? warp_tot[q][tid] : 0u;
+            uint32_t incl = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (tid >= o) incl += t;
+            }
+            __syncwarp();
+            if (tid < kTopkWarps) warp_tot[q][tid] = incl - v;  // exclusive offsets
         }
-        if (tid < kTopkWarps) warp_tot[tid] = incl - v;  // exclusive tie offset per warp
     }
     __syncthreads();
-    uint32_t eq_run = warp_tot[warp_id];
+    uint32_t gt_run = warp_tot[0][warp_id], eq_run = warp_tot[1][warp_id];
     for (int64_t j0 = s0; j0 < s1; j0 += 32) {
         const int64_t j = j0 + lane;
-        uint32_t o = 0;
-        if (j < s1) o = ord_key(src[j]);
+        const uint32_t o = j < s1 ? key_at(j) : 0u;
         const bool gt = j < s1 && o > T, eq = j < s1 && o == T;
         const uint64_t comp = ((uint64_t)o << 32) | (uint32_t)~(uint32_t)j;
+        const uint32_t lt_mask = (1u << lane) - 1u;
         const uint32_t gb = __ballot_sync(0xffffffffu, gt);
-        uint32_t gbase = 0;
-        if (lane == 0 && gb) gbase = atomicAdd(&s_gt, (uint32_t)__popc(gb));
-        gbase = __shfl_sync(0xffffffffu, gbase, 0);
-        if (gt) sel[gbase + __popc(gb & ((1u << lane) - 1u))] = comp;
+        if (gt) sel[gt_run + __popc(gb & lt_mask)] = comp;
+        gt_run += __popc(gb);
         const uint32_t eb = __ballot_sync(0xffffffffu, eq);
-        const uint32_t r = eq_run + __popc(eb & ((1u << lane) - 1u));
+        const uint32_t r = eq_run + __popc(eb & lt_mask);
         if (eq && r < need_eq) sel[G + r] = comp;
         eq_run += __popc(eb);
     }
     __syncthreads();
+    TOPK_TRACE(6);
     int32_t* dst = idx_out + row * k;
-    if (k <= 2048) {
-        // all composites are distinct: output slot = number of selected composites above it
+    if (!sorted) {  // the exact set: strictly-greater then ties, each in index order
+        for (int i = tid; i < k; i += kTopkThreads) dst[i] = (int32_t)(~(uint32_t)sel[i]);
+        if (tid == 0 && counts) counts[row] = (int32_t)k;
+        return;
+    }
+    if (k <= 256) {
+        // small k: all composites are distinct, output slot = number of selected composites
+        // above it (O(k^2 / threads) compares)
         for (int i = tid; i < k; i += kTopkThreads) {
             const uint64_t c = sel[i];
             int rank = 0;
@@ -155,20 +257,8 @@ k_topk_rows(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* __r
     }
     for (int i = (int)k + tid; i < sort_pow2; i += kTopkThreads) sel[i] = 0ull;
     __syncthreads();
-    // bitonic sort, descending
-    for (int size = 2; size <= sort_pow2; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = tid; i < sort_pow2; i += kTopkThreads) {
-                const int partner = i ^ stride;
-                if (partner > i) {
-                    const bool desc = (i & size) == 0;
-                    const uint64_t a = sel[i], b = sel[partner];
-                    if (desc ? (a < b) : (a > b)) { sel[i] = b; sel[partner] = a; }
-                }
-            }
-            __syncthreads();
-        }
-    }
+    bitonic_sort_desc(sel, sort_pow2);
+    TOPK_TRACE(7);
     for (int i = tid; i < k; i += kTopkThreads) dst[i] = (int32_t)(~(uint32_t)sel[i]);
     if (tid == 0 && counts) counts[row] = (int32_t)k;
 }
@@ -203,10 +293,10 @@ __global__ void k_topk_emit_global(const uint64_t* ws, int64_t rows, int64_t k, 
 int64_t topk_max_k() { return kTopkMaxSortK; }
 
 cudaError_t topk_rows(const float* scores, int64_t rows, int64_t m, int64_t k, int32_t* idx,
-                      int32_t* counts, cudaStream_t s) {
+                      int32_t* counts, cudaStream_t s, bool sorted) {
     if (rows == 0) return cudaSuccess;
     if (k > kTopkMaxSortK) return cudaErrorNotSupported;  // caller uses topk_rows_global
-    int p2 = 1;
+    int p2 = 64;  // the register runs of the bitonic sort work on 64-element segments
     while (p2 < k) p2 <<= 1;
     const int stage = m <= kTopkMaxSmemRow ? 1 : 0;
     const size_t smem = sizeof(uint64_t) * p2 + (stage ? sizeof(float) * m : 0);
@@ -215,7 +305,7 @@ cudaError_t topk_rows(const float* scores, int64_t rows, int64_t m, int64_t k, i
         cudaFuncSetAttribute(k_topk_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 196 * 1024);
         attr_set = true;
     }
-    k_topk_rows<<<(unsigned)rows, kTopkThreads, smem, s>>>(scores, m, k, idx, counts, stage, p2);
+    k_topk_rows<<<(unsigned)rows, kTopkThreads, smem, s>>>(scores, m, k, idx, counts, stage, p2, sorted ? 1 : 0);
     return cudaGetLastError();
 }
 
@@ -267,3 +357,9 @@ cudaError_t validate_index_set(const int32_t* idx, const int32_t* counts, int64_
 
 }  // namespace dev
 }  // namespace csd
+
+// Debug only: phase timeline of CTA 0 of the next top-k launches (8 uint64 slots).
+extern "C" int csd_debug_set_topk_trace(void* dev_buf) {
+    uint64_t* p = static_cast<uint64_t*>(dev_buf);
+    return cudaMemcpyToSymbol(csd::dev::g_topk_trace, &p, sizeof(p)) == cudaSuccess ? 0 : 7;
+}
