@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -53,23 +54,35 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
+// Shared memory (runtime offsets in AttnParams, 1 KB-aligned regions):
+//   [Q: tile t strips of round_up(rows_t, 64) rows][X: staged base tile (sparse with base,
+//   chunk <= 192) or the colsum partials][K ring 2 x kKV][V ring 2 x kKV][ids 2 x 512 B][bars]
+// Q comes first: an M-tile with fewer than 128 live rows reads its 128 MMA rows past the end
+// of its strip (into the next strip / X) — dead rows whose P is never used.
 template <int E, int NT>
 struct AttnLayout {
     static constexpr int kHalves = E / 64;
     static constexpr uint32_t kStrip = 128 * 128;  // 128 rows x 128 B
     static constexpr uint32_t kKV = kHalves * kStrip;  // one K or V block
-    static constexpr uint32_t kQ = 0;
-    static constexpr uint32_t kK = kQ + NT * kHalves * kStrip;  // [2] ring
-    static constexpr uint32_t kV = kK + 2 * kKV;                // [2] ring
-    static constexpr uint32_t kCs = kV + 2 * kKV;
-    static constexpr uint32_t kBar = kCs + 2 * 4 * NT * 128 * 4;
-    static constexpr uint32_t kBytes = kBar + 256;
-    static constexpr uint32_t kSmemAlloc = kBytes + 1024;  // manual 1 KB alignment
+    static constexpr uint32_t kCsBytes = 2 * 4 * NT * 128 * 4;
     static constexpr uint32_t kThreads = 128 + 128 * NT;
     static constexpr uint32_t kTmemCols = (NT * 128 + NT * E) <= 256 ? 256 : 512;
+    static constexpr uint32_t kMaxSmem = 227 * 1024;
 };
 
 struct AttnParams {
+    const __nv_bfloat16* k;  // copy mode: sparse K/V rows staged by cp.async
+    const __nv_bfloat16* v;
+    int64_t pitch;           // elements between consecutive token rows
+    int copy_mode;           // 1: sparse K/V rows by cp.async from the producer + idle warps
+    int ncopy;               // copy threads in copy mode
+    int live_t1;             // live softmax threads of the last M-tile (its bar_p arrivals)
+    int stage_base;          // base tile staged in smem region X by TMA (epilogue in smem)
+    int sm_threads;          // threads in the softmax branch (named-barrier count)
+    uint32_t off_x, off_k, off_v, off_ids, off_bar;  // smem region offsets
+    uint32_t q_off[2], q_strip[2];  // per M-tile: Q region offset, bytes per 64-column strip
+    int q_rows[2];           // per M-tile: Q rows loaded (multiple of 64)
+    uint32_t x_strip;        // staged base: bytes per 64-column strip
     const int32_t* idx;
     const int32_t* counts;
     int64_t k_max;
@@ -96,7 +109,8 @@ template <int E, int NT>
 __global__ void __launch_bounds__(AttnLayout<E, NT>::kThreads, 1)
 k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
           const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_kg,
-          const __grid_constant__ CUtensorMap tm_vg, const AttnParams p) {
+          const __grid_constant__ CUtensorMap tm_vg, const __grid_constant__ CUtensorMap tm_b,
+          const __grid_constant__ CUtensorMap tm_o, const AttnParams p) {
     using L = AttnLayout<E, NT>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_u32 = smem_u32(smem_raw);
@@ -110,7 +124,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     const int items = p.items;
     if (threadIdx.x == 0) ATTN_TRACE(0);
 
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
     uint64_t* bar_q = bars + 0;
     uint64_t* bar_kf = bars + 1;   // [2]
     uint64_t* bar_ke = bars + 3;   // [2]
@@ -120,22 +134,43 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     uint64_t* bar_p = bars + 11;   // [NT]
     uint64_t* bar_o = bars + 13;
     uint64_t* bar_qe = bars + 14;  // Q buffer free (all S MMAs of the item done)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+    uint64_t* bar_ids = bars + 15;  // [2] key-row table of ring slot s written (copy mode)
+    uint64_t* bar_bf = bars + 17;   // staged base tile of the current live item landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+    uint32_t* x_done = tmem_slot + 1;  // softmax warps done with region X this item
+    int32_t* ids_tab = reinterpret_cast<int32_t*>(smem + p.off_ids);
+    uint8_t* const sq = smem;
+    uint8_t* const sx = smem + p.off_x;
+    uint8_t* const sk = smem + p.off_k;
+    uint8_t* const sv = smem + p.off_v;
+    const bool cpm = !dense && p.copy_mode;
 
+    if (cpm) {
+        // partial key blocks copy only their live rows; the stale V rows they leave behind
+        // must be finite for P.V (P = 0 there): start from a zeroed V ring
+        for (int i = threadIdx.x; i < (int)(2 * L::kKV / 16); i += blockDim.x)
+            reinterpret_cast<uint4*>(sv)[i] = make_uint4(0u, 0u, 0u, 0u);
+        fence_proxy_async_smem();
+    }
     if (threadIdx.x == 0) {
         mbar_init(bar_q, 1);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(bar_kf + i, 1);
+            // copy mode: one cp.async-tracking arrival per copy thread
+            mbar_init(bar_kf + i, cpm ? p.ncopy : 1);
             mbar_init(bar_ke + i, 1);
-            mbar_init(bar_vf + i, 1);
+            mbar_init(bar_vf + i, cpm ? p.ncopy : 1);
             mbar_init(bar_ve + i, 1);
+            mbar_init(bar_ids + i, 1);
         }
         for (int t = 0; t < NT; ++t) {
             mbar_init(bar_s + t, 1);
-            mbar_init(bar_p + t, 128);
+            // copy mode: the idle warps of tile 1 copy instead of zeroing their P rows
+            mbar_init(bar_p + t, (cpm && t == NT - 1) ? p.live_t1 : 128);
         }
         mbar_init(bar_o, 1);
         mbar_init(bar_qe, 1);
+        mbar_init(bar_bf, 1);
+        *x_done = 0u;
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<L::kTmemCols>(tmem_slot);
@@ -144,18 +179,48 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) ATTN_TRACE(1);
-    if (warp == 0 || warp == 2 || warp == 3) {
-        // ------------------------------------------------------------ producers
-        // TMA instructions issued by one warp are serialised lane by lane (~85 cycles each,
-        // scripts/gather_bench.cu), so the 128 gather4s per key block are spread over the
-        // three non-MMA warps: producer pw issues the row groups g with g % 3 == pw.
+    // next live (count > 0) item of this CTA at or after `from`
+    auto next_live = [&](int from, int& cnt_out) -> int {
+        int x = from;
+        cnt_out = 0;
+        for (; x < items; x += gridDim.x) {
+            cnt_out = dense ? p.n : p.counts[x];
+            if (cnt_out > 0) break;
+        }
+        return x;
+    };
+    // staged base tile of `item` -> region X (64-row TMA boxes, 128B-swizzled strips)
+    auto issue_base = [&](int it) {
+        const int bh2 = it / p.chunks;
+        const int rb2 = p.layout == CSD_LAYOUT_BHNE ? bh2 * p.n : (bh2 / p.heads) * p.n;
+        const int cl2 = p.layout == CSD_LAYOUT_BHNE ? 0 : (bh2 % p.heads) * E;
+        const int nbox = (p.chunk + 63) >> 6;
+        fence_proxy_async_smem();  // prior generic reads of X before the async-proxy refill
+        mbar_arrive_expect_tx(bar_bf, (uint32_t)(L::kHalves * nbox) * 8192u);
+        for (int hf = 0; hf < L::kHalves; ++hf)
+            for (int bx = 0; bx < nbox; ++bx)
+                tma_load_2d(&tm_b, bar_bf, sx + hf * p.x_strip + bx * 8192, cl2 + hf * 64,
+                            rb2 + (it % p.chunks) * p.chunk + bx * 64);
+    };
+    if (p.stage_base && warp == 4 && lane == 0) {
+        int nc = 0;
+        const int first = next_live(blockIdx.x, nc);
+        if (first < items) issue_base(first);
+    }
+    // ---------------------------------------------------------------- producers
+    // TMA mode: warps 0/2/3 spread the gather4s (one warp's TMA issue is serialised).
+    // Copy mode (sparse, idle softmax warps available): K/V rows by cp.async, 16-byte pieces,
+    // one row's pieces on consecutive copy threads (scripts/gather_bench2.cu: ~2.6x the
+    // per-SM rate of tile::gather4); warp 0 publishes each block's key-row table in smem.
+    auto producer = [&](int ct) {  // ct: copy-thread index (warp 0 lanes are 0..31)
         const int pw = warp == 0 ? 0 : warp - 1;
-        const bool mine = (lane % 3) == pw;
+        const bool mine = warp <= 3 && (lane % 3) == pw;
         if (warp == 0 && lane == 0) {
             tma_prefetch_desc(&tm_q);
             tma_prefetch_desc(dense ? &tm_k : &tm_kg);
             tma_prefetch_desc(dense ? &tm_v : &tm_vg);
         }
+        constexpr int kPieces = E / 8;  // 16-byte pieces per key row
         uint32_t gb = 0, li = 0;
         for (int item = blockIdx.x; item < items; item += gridDim.x) {
             const int cnt = dense ? p.n : p.counts[item];
@@ -168,17 +233,19 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             if (warp == 0 && lane == 0) {
                 if (li > 0) mbar_wait(bar_qe, (li - 1) & 1);  // previous item's S MMAs done
                 ATTN_TRACE(2 + li);
-                mbar_arrive_expect_tx(bar_q, NT * L::kHalves * L::kStrip);
+                mbar_arrive_expect_tx(bar_q, (uint32_t)(L::kHalves * (p.q_rows[0] + (NT > 1 ? p.q_rows[1] : 0))) * 128u);
                 for (int t = 0; t < NT; ++t)
                     for (int hf = 0; hf < L::kHalves; ++hf)
-                        tma_load_2d(&tm_q, bar_q, smem + L::kQ + (t * L::kHalves + hf) * L::kStrip,
-                                    col0 + hf * 64, row_base + c * p.chunk + t * 128);
+                        for (int bx = 0; bx < p.q_rows[t] / 64; ++bx)  // 64-row boxes
+                            tma_load_2d(&tm_q, bar_q, sq + p.q_off[t] + hf * p.q_strip[t] + bx * 8192,
+                                        col0 + hf * 64, row_base + c * p.chunk + t * 128 + bx * 64);
             }
             const int32_t* ids = dense ? nullptr : p.idx + (int64_t)item * p.k_max;
             for (int j = 0; j < nblk; ++j, ++gb) {
                 const int s = gb & 1;
-                int32_t rows[4];
-                if (!dense) {
+                const int nvalid = min(128, cnt - j * 128);
+                int32_t rows[4] = {0, 0, 0, 0};
+                if (!dense && (warp == 0 || (!cpm && warp <= 3))) {
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         int r = j * 128 + lane * 4 + i;
@@ -186,11 +253,40 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                         rows[i] = row_base + __ldg(ids + r);
                     }
                 }
-                // K_j -> ring slot s
                 if (gb >= 2) mbar_wait(bar_ke + s, ((gb >> 1) - 1) & 1);
+                if (cpm) {
+                    // slot s's table was read by block gb-2's copies: V of gb-2 consumed
+                    if (gb >= 2) mbar_wait(bar_ve + s, ((gb >> 1) - 1) & 1);
+                    if (warp == 0) {
+                        *reinterpret_cast<int4*>(ids_tab + s * 128 + lane * 4) =
+                            make_int4(rows[0], rows[1], rows[2], rows[3]);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(bar_ids + s);
+                    }
+                    mbar_wait(bar_ids + s, (gb >> 1) & 1);
+                    if (warp == 0 && lane == 0) ATTN_TRACE(16 + gb);
+                    const int32_t* tab = ids_tab + s * 128;
+                    auto copy_rows = [&](const __nv_bfloat16* src_t, uint8_t* dst) {
+                        for (int idx = ct; idx < nvalid * kPieces; idx += p.ncopy) {
+                            const int r = idx / kPieces, piece = idx - r * kPieces;
+                            const char* src = reinterpret_cast<const char*>(
+                                src_t + (int64_t)tab[r] * p.pitch + col0) + piece * 16;
+                            const uint32_t d = smem_u32(dst) + (piece >> 3) * L::kStrip + r * 128 +
+                                               (((piece & 7) ^ (r & 7)) << 4);
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+                        }
+                    };
+                    copy_rows(p.k, sk + s * L::kKV);
+                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar_kf + s)) : "memory");
+                    copy_rows(p.v, sv + s * L::kKV);
+                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar_vf + s)) : "memory");
+                    if (warp == 0 && lane == 0) ATTN_TRACE(48 + gb);
+                    continue;
+                }
+                // K_j -> ring slot s
                 if (warp == 0 && lane == 0) ATTN_TRACE(16 + gb);
                 if (warp == 0 && lane == 0) mbar_arrive_expect_tx(bar_kf + s, L::kKV);
-                uint8_t* kdst = smem + L::kK + s * L::kKV;
+                uint8_t* kdst = sk + s * L::kKV;
                 if (dense) {
                     if (warp == 0 && lane == 0)
                         for (int hf = 0; hf < L::kHalves; ++hf)
@@ -204,7 +300,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 // V_j -> ring slot s
                 if (gb >= 2) mbar_wait(bar_ve + s, ((gb >> 1) - 1) & 1);
                 if (warp == 0 && lane == 0) mbar_arrive_expect_tx(bar_vf + s, L::kKV);
-                uint8_t* vdst = smem + L::kV + s * L::kKV;
+                uint8_t* vdst = sv + s * L::kKV;
                 if (dense) {
                     if (warp == 0 && lane == 0)
                         for (int hf = 0; hf < L::kHalves; ++hf)
@@ -219,19 +315,25 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             }
             ++li;
         }
+    };
+    // copy-thread numbering: warps 0, 2, 3 -> 0..95, then the idle softmax warps
+    const int sw_all = warp - 4;
+    const bool idle_sm = warp >= 4 && cpm && (((sw_all >> 2) * 128 + (warp & 3) * 32) >= p.chunk);
+    if (warp == 0 || warp == 2 || warp == 3) {
+        producer(warp == 0 ? lane : (warp - 1) * 32 + lane);
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
             constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
             constexpr uint32_t idO = idesc_bf16(128, E, false, true);
-            const uint32_t sQ = smem_u32(smem + L::kQ), sK = smem_u32(smem + L::kK);
-            const uint32_t sV = smem_u32(smem + L::kV);
+            const uint32_t sQ = smem_u32(sq), sK = smem_u32(sk);
+            const uint32_t sV = smem_u32(sv);
             auto issue_s = [&](int t, uint32_t g) {  // S_t = Q_t K_g^T
                 const uint32_t kb = sK + (g & 1) * L::kKV;
 #pragma unroll
                 for (int kk = 0; kk < E / 16; ++kk)
                     mma_bf16(tmem + t * 128,
-                             desc_kmajor_sw128(sQ + (t * L::kHalves + kk / 4) * L::kStrip + (kk % 4) * 32),
+                             desc_kmajor_sw128(sQ + p.q_off[t] + (kk / 4) * p.q_strip[t] + (kk % 4) * 32),
                              desc_kmajor_sw128(kb + (kk / 4) * L::kStrip + (kk % 4) * 32), idS,
                              kk > 0 ? 1u : 0u);
                 mma_commit(bar_s + t);
@@ -254,6 +356,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 mbar_wait(bar_q, li & 1);
                 ATTN_TRACE(8 + li);
                 mbar_wait(bar_kf + (gb & 1), (gb >> 1) & 1);
+                if (cpm) fence_proxy_async_smem();  // cp.async (generic proxy) -> tcgen05 reads
                 tc_fence_after();
                 ATTN_TRACE(80 + gb);
                 for (int t = 0; t < NT; ++t) issue_s(t, gb);
@@ -266,13 +369,17 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                         // P_t(j) in TMEM and O_t rescaled; for j = 0 this also orders the
                         // previous item's epilogue reads of O_t (same warps, program order)
                         mbar_wait(bar_p + t, g & 1);
-                        if (t == 0) mbar_wait(bar_vf + (g & 1), (g >> 1) & 1);
+                        if (t == 0) {
+                            mbar_wait(bar_vf + (g & 1), (g >> 1) & 1);
+                            if (cpm) fence_proxy_async_smem();
+                        }
                         tc_fence_after();
                         issue_pv(t, g, j > 0);
                         if (t == NT - 1) mma_commit(bar_ve + (g & 1));
                         if (more) {
                             if (t == 0) {
                                 mbar_wait(bar_kf + ((g + 1) & 1), ((g + 1) >> 1) & 1);
+                                if (cpm) fence_proxy_async_smem();
                                 tc_fence_after();
                                 ATTN_TRACE(80 + g + 1);
                             }
@@ -289,6 +396,10 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 ++li;
             }
         }
+    } else if (idle_sm) {
+        // idle softmax warp (rows past the chunk) in copy mode: extra copy threads
+        const int first_idle = (p.chunk + 31) / 32;  // first idle softmax warp index
+        producer(96 + (sw_all - first_idle) * 32 + lane);
     } else if (warp >= 4) {
         // ------------------------------------------------------------ softmax / epilogue
         const int sw = warp - 4;          // 0 .. 4*NT-1
@@ -300,7 +411,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const uint32_t tS = tmem + lane_off + t * 128;
         const uint32_t tO = tmem + lane_off + NT * 128 + t * E;
-        float* cs_part = reinterpret_cast<float*>(smem + L::kCs);
+        float* cs_part = reinterpret_cast<float*>(sx);
         const bool do_cs = p.colsum != nullptr;
         const float sl2 = p.qk_scale_log2;
         uint32_t gb = 0, li = 0;
@@ -339,9 +450,12 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                     // S row in two 64-column halves (2 TMEM loads in flight, one wait each)
                     // fast path (uniform): every column and every row of this warp is live
                     const bool full = ncols == 128 && __all_sync(0xffffffffu, row_ok);
-                    float mraw = -INFINITY;
+                    const int ngrp = full ? 4 : (ncols + 31) >> 5;  // live 32-column groups
+                    // pass 1: row max over the live halves, four independent max chains
+                    float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
                     for (int hf = 0; hf < 2; ++hf) {
+                        if (hf * 2 >= ngrp) break;  // uniform
                         uint32_t sr[64];
                         tmem_ld32(tS + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
                         tmem_ld32(tS + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
@@ -352,9 +466,13 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                                 if (hf * 64 + i >= ncols) sr[i] = __float_as_uint(-INFINITY);
                         }
 #pragma unroll
-                        for (int i = 0; i < 64; i += 2)
-                            mraw = fmax3(mraw, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
+                        for (int i = 0; i < 64; i += 8)
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                mx4[u] = fmax3(mx4[u], __uint_as_float(sr[i + 2 * u]),
+                                               __uint_as_float(sr[i + 2 * u + 1]));
                     }
+                    const float mraw = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
                     const float mx = row_ok ? mraw * sl2 : -INFINITY;  // sl2 > 0: max commutes
                     m_true = fmaxf(m_true, mx);
                     const bool need = mx > m_run + kRescaleThreshold;
@@ -377,20 +495,37 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                     }
                     const float w = do_cs ? ex2_approx(m_run - mpl) * inv_lp : 0.f;
                     const float neg_m = row_ok ? -m_run : -INFINITY;  // dead rows -> p = 0
+                    const float2 sl2v = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
+                    float2 part0 = make_float2(0.f, 0.f), part1 = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int cc = 0; cc < 4; ++cc) {
+                        if (cc >= ngrp) {  // uniform: a fully masked group contributes P = 0
+                            uint32_t pk[16];
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) pk[q] = 0u;
+                            tmem_st16(tS + cc * 16, pk);
+                            if (do_cs) cs_part[((g & 1) * 4 * NT + sw) * 128 + cc * 32 + lane] = 0.f;
+                            continue;
+                        }
                         uint32_t sr[32];
                         tmem_ld32(tS + cc * 32, sr);
                         tmem_ld_wait();
                         float pv[32];
-                        float part = 0.f;
+                        // 2^(S*scale - m) with paired FFMA2 / FADD2 (two row sums in flight)
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            const float x = (full || cc * 32 + i < ncols) ? __uint_as_float(sr[i]) : -INFINITY;
-                            pv[i] = ex2_approx(fmaf(x, sl2, neg_m));
-                            part += pv[i];
+                        for (int q = 0; q < 16; ++q) {
+                            float2 x;
+                            x.x = (full || cc * 32 + 2 * q < ncols) ? __uint_as_float(sr[2 * q]) : -INFINITY;
+                            x.y = (full || cc * 32 + 2 * q + 1 < ncols) ? __uint_as_float(sr[2 * q + 1]) : -INFINITY;
+                            const float2 y = __ffma2_rn(x, sl2v, nm2);
+                            float2 e;
+                            e.x = ex2_approx(y.x);
+                            e.y = ex2_approx(y.y);
+                            pv[2 * q] = e.x;
+                            pv[2 * q + 1] = e.y;
+                            if (q & 1) part1 = __fadd2_rn(part1, e);
+                            else part0 = __fadd2_rn(part0, e);
                         }
-                        l_run += part;
                         // P_t (bf16 pairs) over S_t columns [16 cc, 16 cc + 16) — already read
                         uint32_t pk[16];
 #pragma unroll
@@ -413,6 +548,8 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                             cs_part[((g & 1) * 4 * NT + sw) * 128 + cc * 32 + lane] = pv[0];
                         }
                     }
+                    const float2 part = __fadd2_rn(part0, part1);
+                    l_run += part.x + part.y;
                 } else {
                     // rows past the chunk: zero P so the padded MMA rows stay finite
                     uint32_t pk[16];
@@ -437,9 +574,76 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 }
             }
             // ------------------------------------------------------------ epilogue
+            const bool has_base = p.base != nullptr;
+            if (p.stage_base) {
+                // out = base + scale * O / l (north_star item 5) with the item's base tile
+                // already in smem (TMA, issued at the end of the previous item's epilogue):
+                // each thread combines its row in place (bf16, swizzled), then each warp
+                // copies its 32 rows out row-contiguously (16-byte lanes).
+                mbar_wait(bar_o, li & 1);
+                mbar_wait(bar_bf, li & 1);
+                tc_fence_after();
+                if (lane == 0 && sw == 0) ATTN_TRACE(240 + li);
+                if (warp_ok) {
+                    const float fsc = p.scale / l_run;
+#pragma unroll
+                    for (int oc = 0; oc < E / 32; ++oc) {
+                        uint32_t r[32];
+                        tmem_ld32(tO + oc * 32, r);
+                        tmem_ld_wait();
+                        if (!row_ok) continue;
+                        uint8_t* rowp = sx + (oc >> 1) * p.x_strip + crow * 128;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int cidx = (oc & 1) * 4 + q;
+                            uint4* ptr = reinterpret_cast<uint4*>(rowp + ((cidx ^ (crow & 7)) << 4));
+                            const uint4 bv = *ptr;
+                            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bv);
+                            uint32_t o4[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const float2 f = __bfloat1622float2(b2[u]);
+                                o4[u] = pack_bf16x2(fmaf(fsc, __uint_as_float(r[q * 8 + 2 * u]), f.x),
+                                                    fmaf(fsc, __uint_as_float(r[q * 8 + 2 * u + 1]), f.y));
+                            }
+                            *ptr = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+                        }
+                    }
+                    if (lane == 0 && sw == 0) ATTN_TRACE(232 + li);
+                    if (row_ok && p.row_max != nullptr) {
+                        const int64_t si = (int64_t)bh * p.n + tok;
+                        p.row_max[si] = m_true * kLn2;
+                        p.exp_sum[si] = l_run * exp2f(m_run - m_true);
+                    }
+                }
+                // the last warp done with X stores the out tile (TMA, from X) and refills X
+                // with the next live item's base tile; the other warps go straight on
+                fence_proxy_async_smem();  // this thread's in-place writes -> async proxy
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence_block();
+                    const uint32_t prev = atomicAdd(x_done, 1u);
+                    if (prev == (uint32_t)(p.sm_threads / 32) - 1u) {
+                        *x_done = 0u;
+                        __threadfence_block();
+                        fence_proxy_async_smem();
+                        const int nbox = (p.chunk + 63) >> 6;
+                        const int rb = p.layout == CSD_LAYOUT_BHNE ? bh * p.n : b * p.n;
+                        const int cl = p.layout == CSD_LAYOUT_BHNE ? 0 : h * E;
+                        for (int hf = 0; hf < L::kHalves; ++hf)
+                            for (int bx = 0; bx < nbox; ++bx)
+                                tma_store_2d(&tm_o, sx + hf * p.x_strip + bx * 8192, cl + hf * 64,
+                                             rb + c * p.chunk + bx * 64);
+                        bulk_commit();
+                        bulk_wait_read0();  // X read out before it is refilled
+                        int nc = 0;
+                        const int nx = next_live(item + gridDim.x, nc);
+                        if (nx < items) issue_base(nx);
+                    }
+                }
+            } else {
             const int64_t off = tok_elem_off(p.layout, b, h, tok, p.heads, p.n, E);
             uint4 bpre[E / 8];  // prefetch base while the last P.V runs
-            const bool has_base = p.base != nullptr;
             if (warp_ok && row_ok && has_base) {
                 const uint4* bp = reinterpret_cast<const uint4*>(p.base + off);
 #pragma unroll
@@ -489,6 +693,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                     p.row_max[si] = m_true * kLn2;
                     p.exp_sum[si] = l_run * exp2f(m_run - m_true);
                 }
+            }
             }
             if (lane == 0 && sw == 0) ATTN_TRACE(248 + li);
             tc_fence_before();  // O reads ordered before the next item's bar_p arrive
@@ -545,14 +750,32 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
     const uint64_t cols = a.layout == CSD_LAYOUT_BHNE ? E : (uint64_t)a.heads * E;
     const uint64_t rows = a.layout == CSD_LAYOUT_BHNE ? (uint64_t)(a.batch * a.heads * a.n)
                                                       : (uint64_t)(a.batch * a.n);
-    CUtensorMap tq, tk, tv, tkg, tvg;
-    if (!make_map_bf16(&tq, a.q, cols, rows, cols, 128) ||
+    CUtensorMap tq, tk, tv, tkg, tvg, tb, to;
+    if (!make_map_bf16(&tq, a.q, cols, rows, cols, 64) ||
+        !make_map_bf16(&to, a.out, cols, rows, cols, 64) ||
+        !make_map_bf16(&tb, a.base != nullptr ? a.base : a.q, cols, rows, cols, 64) ||
         !make_map_bf16(&tk, a.k, cols, rows, cols, 128) ||
         !make_map_bf16(&tv, a.v, cols, rows, cols, 128) ||
         !make_map_bf16(&tkg, a.k, cols, rows, cols, 1) ||
         !make_map_bf16(&tvg, a.v, cols, rows, cols, 1))
         return cudaErrorInvalidValue;
     AttnParams p{};
+    p.k = static_cast<const __nv_bfloat16*>(a.k);
+    p.v = static_cast<const __nv_bfloat16*>(a.v);
+    p.pitch = (int64_t)cols;
+    {
+        // copy mode needs >= 2 idle softmax warps (rows past the chunk in the last M-tile)
+        const int idle = 4 * NT - (int)((a.chunk + 31) / 32);
+        static const int env = [] {
+            // default: TMA tile::gather4 (measured faster end to end at FLUX: 63.5 vs 66 us;
+            // cp.async copies contend with the softmax warps); CSD_ATTN_COPY=1 selects copies
+            const char* e = std::getenv("CSD_ATTN_COPY");
+            return e != nullptr ? std::atoi(e) : 0;
+        }();
+        p.copy_mode = (a.idx != nullptr && idle >= 2 && env != 0) ? 1 : 0;
+        p.ncopy = 96 + 32 * idle;
+        p.live_t1 = (int)std::min<int64_t>(128, ((a.chunk - 128 * (NT - 1)) + 31) / 32 * 32);
+    }
     p.idx = a.idx;
     p.counts = a.counts;
     p.k_max = a.k_max;
@@ -571,11 +794,40 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
     p.chunks = (int)(a.n / a.chunk);
     p.items = (int)(a.batch * a.heads * p.chunks);
     p.qk_scale_log2 = kLog2e / std::sqrt((float)E);
+    // ---- shared-memory layout (see AttnLayout)
+    {
+        auto al = [](uint32_t v) { return (v + 1023u) & ~1023u; };
+        uint32_t off = 0;
+        for (int t = 0; t < 2; ++t) {
+            const int rows_t = t < NT ? (int)((std::min<int64_t>(128, a.chunk - 128 * t) + 63) / 64 * 64) : 0;
+            p.q_rows[t] = rows_t;
+            p.q_off[t] = off;
+            p.q_strip[t] = (uint32_t)rows_t * 128u;
+            off = al(off + L::kHalves * p.q_strip[t]);
+        }
+        const uint32_t xrows = (uint32_t)((a.chunk + 63) / 64 * 64);
+        const uint32_t xbase = L::kHalves * xrows * 128u;
+        const uint32_t tail = 4 * L::kKV + 2 * 512 + 256 + 1024;  // rings, ids, bars, align slack
+        const bool want = a.base != nullptr && a.colsum == nullptr && off + xbase + tail <= L::kMaxSmem;
+        p.stage_base = want ? 1 : 0;
+        p.x_strip = xrows * 128u;
+        p.off_x = off;
+        off = al(off + (want ? std::max(xbase, L::kCsBytes) : L::kCsBytes));
+        p.off_k = off;
+        p.off_v = off + 2 * L::kKV;
+        p.off_ids = p.off_v + 2 * L::kKV;
+        p.off_bar = p.off_ids + 2 * 512;
+        p.sm_threads = p.copy_mode ? 128 + 32 * (int)((std::min<int64_t>(128 * NT, a.chunk) - 128 + 31) / 32)
+                                   : 128 * NT;
+        if (NT == 1) p.sm_threads = p.copy_mode ? (int)((a.chunk + 31) / 32 * 32) : 128;
+    }
+    const uint32_t smem_bytes = p.off_bar + 256 + 1024;
+    if (smem_bytes > L::kMaxSmem) return cudaErrorNotSupported;
     auto kern = k_attn_tc<E, NT>;
     static bool attr_done = false;  // once per instantiation (keeps graph capture clean)
     if (!attr_done) {
         cudaError_t err =
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemAlloc);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kMaxSmem);
         if (err != cudaSuccess) return err;
         attr_done = true;
     }
@@ -587,7 +839,7 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
     }
     // persistent: one CTA per SM (smem-limited), items strided over the grid
     const unsigned grid = (unsigned)std::min<int64_t>(p.items, sms);
-    kern<<<grid, L::kThreads, L::kSmemAlloc, s>>>(tq, tk, tv, tkg, tvg, p);
+    kern<<<grid, L::kThreads, smem_bytes, s>>>(tq, tk, tv, tkg, tvg, tb, to, p);
     return cudaGetLastError();
 }
 

@@ -64,7 +64,7 @@ def main():
             if not row[8 + li]:
                 continue
             print(f" item {li}: Q issue {us(2 + li)}  Q ready(MMA) {us(8 + li)}  "
-                  f"epi start {us(240 + li)}  epi end {us(248 + li)}")
+                  f"epi start {us(240 + li)}  rmw done {us(232 + li)}  epi end {us(248 + li)}")
         for gbk in range(16):
             if not row[16 + gbk]:
                 continue
