@@ -43,6 +43,12 @@ using namespace csd::tc;
 // stamps at fixed slots (start, Q / K / V issue, S issue, softmax and epilogue phases).
 constexpr int kTraceCtas = 8, kTraceSlots = 256;
 __device__ uint64_t* g_attn_trace = nullptr;
+__device__ uint64_t* g_attn_span = nullptr;  // [grid][2] globaltimer at CTA start / end
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 #define ATTN_TRACE(slot)                                                                  \
     do {                                                                                  \
         uint64_t* tr_ = g_attn_trace;                                                     \
@@ -78,7 +84,8 @@ struct AttnParams {
     int ncopy;               // copy threads in copy mode
     int live_t1;             // live softmax threads of the last M-tile (its bar_p arrivals)
     int stage_base;          // base tile staged in smem region X by TMA (epilogue in smem)
-    int sm_threads;          // threads in the softmax branch (named-barrier count)
+    int sm_threads;          // threads in the softmax branch (barrier counts), TMA mode
+    int sm_threads_copy;     // ... in copy mode (idle softmax warps copy instead)
     uint32_t off_x, off_k, off_v, off_ids, off_bar;  // smem region offsets
     uint32_t q_off[2], q_strip[2];  // per M-tile: Q region offset, bytes per 64-column strip
     int q_rows[2];           // per M-tile: Q rows loaded (multiple of 64)
@@ -123,6 +130,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     const bool dense = p.idx == nullptr;
     const int items = p.items;
     if (threadIdx.x == 0) ATTN_TRACE(0);
+    if (threadIdx.x == 0 && g_attn_span != nullptr) g_attn_span[2 * blockIdx.x] = globaltimer_ns();
 
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
     uint64_t* bar_q = bars + 0;
@@ -136,14 +144,16 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     uint64_t* bar_qe = bars + 14;  // Q buffer free (all S MMAs of the item done)
     uint64_t* bar_ids = bars + 15;  // [2] key-row table of ring slot s written (copy mode)
     uint64_t* bar_bf = bars + 17;   // staged base tile of the current live item landed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
-    uint32_t* x_done = tmem_slot + 1;  // softmax warps done with region X this item
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+    uint64_t* bar_xc = bars + 19;   // every live softmax warp combined its rows into X
     int32_t* ids_tab = reinterpret_cast<int32_t*>(smem + p.off_ids);
     uint8_t* const sq = smem;
     uint8_t* const sx = smem + p.off_x;
     uint8_t* const sk = smem + p.off_k;
     uint8_t* const sv = smem + p.off_v;
-    const bool cpm = !dense && p.copy_mode;
+    // copy_mode 2: odd CTAs copy (LSU), even CTAs gather (TMA) -- TPC siblings split the paths
+    const bool cpm = !dense && (p.copy_mode == 1 || (p.copy_mode == 2 && (blockIdx.x & 1)));
+    const int sm_threads = cpm ? p.sm_threads_copy : p.sm_threads;
 
     if (cpm) {
         // partial key blocks copy only their live rows; the stale V rows they leave behind
@@ -170,7 +180,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         mbar_init(bar_o, 1);
         mbar_init(bar_qe, 1);
         mbar_init(bar_bf, 1);
-        *x_done = 0u;
+        mbar_init(bar_xc, sm_threads / 32);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<L::kTmemCols>(tmem_slot);
@@ -202,11 +212,34 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 tma_load_2d(&tm_b, bar_bf, sx + hf * p.x_strip + bx * 8192, cl2 + hf * 64,
                             rb2 + (it % p.chunks) * p.chunk + bx * 64);
     };
-    if (p.stage_base && warp == 4 && lane == 0) {
+    // staged-base I/O thread (warp 1 lane 1; lane 0 issues the MMAs): per live item, base
+    // tile in, then -- once every softmax warp has combined its rows in place -- the out tile
+    // out by TMA store, then the next item's base tile in
+    auto io_thread = [&]() {
         int nc = 0;
-        const int first = next_live(blockIdx.x, nc);
-        if (first < items) issue_base(first);
-    }
+        int it = next_live(blockIdx.x, nc);
+        if (it < items) issue_base(it);
+        uint32_t li = 0;
+        while (it < items) {
+            const int bh2 = it / p.chunks, c2 = it % p.chunks;
+            const int rb = p.layout == CSD_LAYOUT_BHNE ? bh2 * p.n : (bh2 / p.heads) * p.n;
+            const int cl = p.layout == CSD_LAYOUT_BHNE ? 0 : (bh2 % p.heads) * E;
+            const int nx = next_live(it + gridDim.x, nc);
+            mbar_wait(bar_xc, li & 1);
+            fence_proxy_async_smem();
+            const int nbox = (p.chunk + 63) >> 6;
+            for (int hf = 0; hf < L::kHalves; ++hf)
+                for (int bx = 0; bx < nbox; ++bx)
+                    tma_store_2d(&tm_o, sx + hf * p.x_strip + bx * 8192, cl + hf * 64,
+                                 rb + c2 * p.chunk + bx * 64);
+            bulk_commit();
+            bulk_wait_read0();  // X read out before it is refilled
+            if (nx < items) issue_base(nx);
+            it = nx;
+            ++li;
+        }
+        bulk_wait0();  // the last out tile has landed before the CTA exits
+    };
     // ---------------------------------------------------------------- producers
     // TMA mode: warps 0/2/3 spread the gather4s (one warp's TMA issue is serialised).
     // Copy mode (sparse, idle softmax warps available): K/V rows by cp.async, 16-byte pieces,
@@ -322,6 +355,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     if (warp == 0 || warp == 2 || warp == 3) {
         producer(warp == 0 ? lane : (warp - 1) * 32 + lane);
     } else if (warp == 1) {
+        if (lane == 1 && p.stage_base) io_thread();
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
             constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
@@ -616,31 +650,11 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                         p.exp_sum[si] = l_run * exp2f(m_run - m_true);
                     }
                 }
-                // the last warp done with X stores the out tile (TMA, from X) and refills X
-                // with the next live item's base tile; the other warps go straight on
+                // hand X to the I/O thread (warp 1 lane 1): it stores the out tile by TMA and
+                // refills X with the next live item's base tile; the softmax warps go on
                 fence_proxy_async_smem();  // this thread's in-place writes -> async proxy
                 __syncwarp();
-                if (lane == 0) {
-                    __threadfence_block();
-                    const uint32_t prev = atomicAdd(x_done, 1u);
-                    if (prev == (uint32_t)(p.sm_threads / 32) - 1u) {
-                        *x_done = 0u;
-                        __threadfence_block();
-                        fence_proxy_async_smem();
-                        const int nbox = (p.chunk + 63) >> 6;
-                        const int rb = p.layout == CSD_LAYOUT_BHNE ? bh * p.n : b * p.n;
-                        const int cl = p.layout == CSD_LAYOUT_BHNE ? 0 : h * E;
-                        for (int hf = 0; hf < L::kHalves; ++hf)
-                            for (int bx = 0; bx < nbox; ++bx)
-                                tma_store_2d(&tm_o, sx + hf * p.x_strip + bx * 8192, cl + hf * 64,
-                                             rb + c * p.chunk + bx * 64);
-                        bulk_commit();
-                        bulk_wait_read0();  // X read out before it is refilled
-                        int nc = 0;
-                        const int nx = next_live(item + gridDim.x, nc);
-                        if (nx < items) issue_base(nx);
-                    }
-                }
+                if (lane == 0) mbar_arrive(bar_xc);
             } else {
             const int64_t off = tok_elem_off(p.layout, b, h, tok, p.heads, p.n, E);
             uint4 bpre[E / 8];  // prefetch base while the last P.V runs
@@ -703,6 +717,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0 && g_attn_span != nullptr) g_attn_span[2 * blockIdx.x + 1] = globaltimer_ns();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<L::kTmemCols>(tmem);
@@ -772,7 +787,7 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
             const char* e = std::getenv("CSD_ATTN_COPY");
             return e != nullptr ? std::atoi(e) : 0;
         }();
-        p.copy_mode = (a.idx != nullptr && idle >= 2 && env != 0) ? 1 : 0;
+        p.copy_mode = (a.idx != nullptr && idle >= 2) ? env : 0;
         p.ncopy = 96 + 32 * idle;
         p.live_t1 = (int)std::min<int64_t>(128, ((a.chunk - 128 * (NT - 1)) + 31) / 32 * 32);
     }
@@ -817,9 +832,9 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
         p.off_v = off + 2 * L::kKV;
         p.off_ids = p.off_v + 2 * L::kKV;
         p.off_bar = p.off_ids + 2 * 512;
-        p.sm_threads = p.copy_mode ? 128 + 32 * (int)((std::min<int64_t>(128 * NT, a.chunk) - 128 + 31) / 32)
-                                   : 128 * NT;
-        if (NT == 1) p.sm_threads = p.copy_mode ? (int)((a.chunk + 31) / 32 * 32) : 128;
+        // softmax-branch threads without / with copy mode (idle warps become copy threads)
+        p.sm_threads = 128 * NT;
+        p.sm_threads_copy = (int)((std::min<int64_t>(128 * NT, a.chunk) + 31) / 32 * 32);
     }
     const uint32_t smem_bytes = p.off_bar + 256 + 1024;
     if (smem_bytes > L::kMaxSmem) return cudaErrorNotSupported;
@@ -859,4 +874,9 @@ cudaError_t attn_tc(const AttnTcArgs& a, cudaStream_t s) {
 extern "C" int csd_debug_set_attn_trace(void* dev_buf) {
     uint64_t* p = static_cast<uint64_t*>(dev_buf);
     return cudaMemcpyToSymbol(csd::dev::g_attn_trace, &p, sizeof(p)) == cudaSuccess ? 0 : 7;
+}
+// Debug only: per-CTA [start, end] globaltimer stamps (2 x grid uint64).
+extern "C" int csd_debug_set_attn_span(void* dev_buf) {
+    uint64_t* p = static_cast<uint64_t*>(dev_buf);
+    return cudaMemcpyToSymbol(csd::dev::g_attn_span, &p, sizeof(p)) == cudaSuccess ? 0 : 7;
 }

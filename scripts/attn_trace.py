@@ -52,6 +52,20 @@ def main():
     torch.cuda.synchronize()
     fn(None)
     print("launch %.1f us (traced)" % (ev0.elapsed_time(ev1) * 1e3))
+    # untraced launch with per-CTA spans
+    fs = lib.csd_debug_set_attn_span
+    fs.argtypes = [ctypes.c_void_p]
+    span = torch.zeros(2 * 148, dtype=torch.int64, device="cuda")
+    fs(span.data_ptr())
+    ops.sparse_delta_attention(q, k, v, idx, base, 1.0, layout=1, out=out)
+    torch.cuda.synchronize()
+    fs(None)
+    sp = span.view(148, 2).cpu().tolist()
+    t0 = min(a for a, _ in sp)
+    ends = sorted(((e - t0) / 1e3, i) for i, (_, e) in enumerate(sp))
+    print("CTA end times (us): min %.1f  median %.1f  max %.1f; slowest CTAs %s" % (
+        ends[0][0], ends[len(ends) // 2][0], ends[-1][0], [i for _, i in ends[-6:]]))
+    print("  start spread %.1f us" % ((max(a for a, _ in sp) - t0) / 1e3))
     t = buf.view(8, SLOTS).cpu().tolist()
     for cta in range(args.ctas):
         row = t[cta]

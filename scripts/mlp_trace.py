@@ -38,11 +38,10 @@ for cta in range(2):
     print("  k-block issue :", " ".join(f"{us(2 + k):.1f}" for k in range(0, 48, 4)))
     print("  k-block ready :", " ".join(f"{us(64 + k):.1f}" for k in range(0, 48, 4)))
     print(f"  epilogue: act tile landed {us(130):.2f}  math done {us(131):.2f}")
-print("k_smlp_down (CTAs x<8 of chunk 0):")
-for cta in range(3):
-    r = t[cta]
-    t0 = r[200]
-    us = lambda s: (r[s] - t0) / 1965.0 if r[s] else float("nan")  # noqa: E731
-    print(f"CTA {cta}: setup {us(201):.2f} k-blocks ready " +
-          " ".join(f"{us(202 + k):.1f}" for k in range(14)) +
-          f" | epilogue {us(230):.2f} -> {us(231):.2f}")
+print("k_smlp_down, CTA 0 (persistent items):")
+r = t[0]
+t0 = r[200]
+us = lambda s: (r[s] - t0) / 1965.0 if r[s] else float("nan")  # noqa: E731
+for li in range(5):
+    print(f"  item {li}: K loop {us(202 + 2 * li):6.2f} -> {us(203 + 2 * li):6.2f} | epilogue "
+          f"{us(230 + 2 * li):6.2f} -> {us(231 + 2 * li):6.2f}")
