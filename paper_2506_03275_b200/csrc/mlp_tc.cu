@@ -232,9 +232,13 @@ k_smlp_up(const __grid_constant__ CUtensorMap tm_x, const MlpParams p) {
             if (kb >= nst) mbar_wait(empty + s, ((kb / nst) - 1) & 1);
             if (warp == 0 && lane == 0) {
                 MLP_TRACE(2 + kb);
-                mbar_arrive_expect_tx(full + s, NT * kTile);
-                for (int t = 0; t < NT; ++t)
-                    tma_load_2d(&tm_x, full + s, smem + s * sbytes + t * kTile, kb * 64, x_row0 + t * 128);
+                // only the chunk's rows (64-row boxes); the MMA's rows past the chunk read
+                // stale smem -- dead accumulator rows that are never stored
+                const int nbox = (p.chunk + 63) >> 6;
+                mbar_arrive_expect_tx(full + s, (uint32_t)nbox * 8192u);
+                for (int bx = 0; bx < nbox; ++bx)
+                    tma_load_2d(&tm_x, full + s, smem + s * sbytes + (bx >> 1) * kTile + (bx & 1) * 8192,
+                                kb * 64, x_row0 + bx * 64);
             }
 #pragma unroll
             for (int i = 0; i < kPer; ++i)
@@ -454,10 +458,11 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
                 }
                 if (gk >= kDnStages) mbar_wait(empty + s, ((gk / kDnStages) - 1) & 1);
                 if (warp == 0 && lane == 0) {
-                    mbar_arrive_expect_tx(full + s, NT * kTile);
-                    for (int t = 0; t < NT; ++t)
-                        tma_load_2d(&tm_delta, full + s, smem + s * L::kStage + t * kTile, kb * 64,
-                                    z * p.chunk + t * 128);
+                    const int nbox = (p.chunk + 63) >> 6;  // only the chunk's rows
+                    mbar_arrive_expect_tx(full + s, (uint32_t)nbox * 8192u);
+                    for (int bx = 0; bx < nbox; ++bx)
+                        tma_load_2d(&tm_delta, full + s, smem + s * L::kStage + (bx >> 1) * kTile + (bx & 1) * 8192,
+                                    kb * 64, z * p.chunk + bx * 64);
                 }
 #pragma unroll
                 for (int i = 0; i < kPer; ++i) {
@@ -612,8 +617,8 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
     int tn_width = 0, ntiles = 0;
     smlp_geometry(k_max, batch * nc, &tn_width, &ntiles, nullptr);
     CUtensorMap tx, tdl;
-    if (!make_map_bf16(&tx, x, d, batch * n, d, 128) ||
-        !make_map_bf16(&tdl, delta_ws, k_pad, batch * nc * chunk, k_pad, 128))
+    if (!make_map_bf16(&tx, x, d, batch * n, d, 64) ||
+        !make_map_bf16(&tdl, delta_ws, k_pad, batch * nc * chunk, k_pad, 64))
         return cudaErrorInvalidValue;
     MlpParams p{};
     p.w1 = (const __nv_bfloat16*)w1;
