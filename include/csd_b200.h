@@ -80,6 +80,11 @@ csd_status csd_copy_to_host(void* dst, const void* src, size_t bytes);
 /* PROD-mode index-set validation on every sparse call (default on; the block
  * runner disables it for its own top-k sets, which are valid by construction). */
 csd_status csd_ctx_set_validation(csd_ctx* ctx, int enabled);
+/* select_top_k output order (default 1: descending score, lower index first on ties,
+ * sparse_index.cpp:86-90).  0: the same exact index SET, strictly-greater entries then the
+ * lowest-index ties, each in index order (what the PROD block path uses: its consumers are
+ * order-invariant; lets few long rows run as a cluster of CTAs per row). */
+csd_status csd_ctx_set_sorted_topk(csd_ctx* ctx, int sorted);
 /* Number of kernels this context launched since creation (instrumentation). */
 int64_t csd_ctx_launch_count(const csd_ctx* ctx);
 

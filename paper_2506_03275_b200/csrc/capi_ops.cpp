@@ -105,6 +105,12 @@ csd_status csd_ctx_set_validation(csd_ctx* ctx, int enabled) {
     return CSD_OK;
 }
 
+csd_status csd_ctx_set_sorted_topk(csd_ctx* ctx, int sorted) {
+    if (!ctx) return set_error(CSD_ERR_VALUE, "null context");
+    reinterpret_cast<Ctx*>(ctx)->sorted_topk = sorted != 0;
+    return CSD_OK;
+}
+
 // ---------------------------------------------------------------- attention
 csd_status csd_dense_attention(csd_ctx* ctx, csd_mode mode, csd_layout layout, const void* q,
                                const void* k, const void* v, int64_t batch, int64_t heads,

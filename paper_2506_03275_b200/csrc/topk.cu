@@ -33,6 +33,10 @@ constexpr int kTopkWarps = kTopkThreads / 32;
 constexpr int64_t kTopkMaxSortK = 16384;         // 128 KB of u64 composites
 constexpr int64_t kTopkMaxSmemRow = 16 * 1024;  // fp32 elements staged in smem
 
+__device__ __forceinline__ uint32_t smem_u32_generic(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 __device__ __forceinline__ uint32_t ord_key(float x) {
     uint32_t u = __float_as_uint(x);
     if ((u << 1) == 0) u = 0;  // -0.0 == +0.0
@@ -263,6 +267,205 @@ k_topk_rows(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* __r
     if (tid == 0 && counts) counts[row] = (int32_t)k;
 }
 
+// ---------------------------------------------------------------------------
+// Cluster top-k for few, long rows (the MLP selection: 24 rows x 12288 at FLUX would keep
+// only 24 SMs busy): a cluster of CS CTAs shares one row.  Each CTA owns a contiguous
+// segment (its warps contiguous sub-segments, so index order = (CTA, warp, lane) order);
+// every radix pass builds per-warp histograms, sums them per CTA, and every CTA reads all
+// CTAs' histograms through distributed shared memory to take the same digit decision.  The
+// per-CTA / per-warp counts above the selected digit accumulate into exact gt / eq offsets,
+// so one write pass emits the index SET (strictly greater, then the lowest-index ties), each
+// part in index order.  Unsorted output only (the PROD block path).
+__device__ __forceinline__ uint32_t dsmem_ld(const uint32_t* local_addr, uint32_t cta) {
+    uint32_t raddr, v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32_generic(local_addr)), "r"(cta));
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(raddr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+template <int CS>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kTopkThreads)
+k_topk_cluster(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* __restrict__ idx_out,
+               int32_t* __restrict__ counts) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint32_t* keys = reinterpret_cast<uint32_t*>(smem);  // this CTA's segment
+    __shared__ uint32_t whist[kTopkWarps][256];
+    __shared__ uint32_t chist[2][256];        // this CTA's histogram, double-buffered by pass
+    __shared__ uint32_t red[2];               // AND / OR of this CTA's keys
+    __shared__ uint32_t s_prefix, s_kleft, s_sel, s_shift;
+    __shared__ uint32_t cta_gt[CS], warp_gt[kTopkWarps], warp_eq[kTopkWarps], cta_eq[CS];
+    __shared__ uint32_t tot_bins[256];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t rank = cluster_rank();
+    const int64_t row = blockIdx.x / CS;
+    const float* src = scores + row * m;
+    TOPK_TRACE(0);
+    const int64_t seg = (m + CS - 1) / CS;
+    const int64_t c0 = (int64_t)rank * seg, c1 = min(m, c0 + seg);
+    const int64_t nloc = max((int64_t)0, c1 - c0);
+    const int64_t wseg = (nloc + kTopkWarps - 1) / kTopkWarps;  // per-warp sub-segment
+    const int64_t w0 = min(nloc, warp * wseg), w1 = min(nloc, w0 + wseg);
+    uint32_t kand = 0xffffffffu, kor = 0u;
+    for (int64_t j = w0 + lane; j < w1; j += 32) {
+        const uint32_t o = ord_key(src[c0 + j]);
+        keys[j] = o;
+        kand &= o;
+        kor |= o;
+    }
+    kand = __reduce_and_sync(0xffffffffu, kand);
+    kor = __reduce_or_sync(0xffffffffu, kor);
+    if (lane == 0) { whist[0][warp] = kand; whist[1][warp] = kor; }
+    if (tid < CS) { cta_gt[tid] = 0; cta_eq[tid] = 0; }
+    if (tid < kTopkWarps) warp_gt[tid] = 0;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t a = 0xffffffffu, o = 0u;
+        for (int w = 0; w < kTopkWarps; ++w) { a &= whist[0][w]; o |= whist[1][w]; }
+        red[0] = a;
+        red[1] = o;
+    }
+    cluster_sync_all();
+    if (tid == 0) {
+        uint32_t a = 0xffffffffu, o = 0u;
+        for (uint32_t r = 0; r < CS; ++r) { a &= dsmem_ld(&red[0], r); o |= dsmem_ld(&red[1], r); }
+        const int lead = __clz(a ^ o);
+        s_prefix = lead >= 32 ? a : (a & ~(0xffffffffu >> lead));
+        s_kleft = (uint32_t)k;
+        s_shift = (uint32_t)lead;
+    }
+    __syncthreads();
+    const int lead = (int)s_shift;
+    TOPK_TRACE(1);
+    uint32_t mask = lead >= 32 ? 0xffffffffu : ~(0xffffffffu >> lead);
+    int pass = 0;
+    for (int top = 32 - lead; top > 0; top -= 8, ++pass) {
+        const int nb = min(8, top), shift = top - nb;
+        const uint32_t dmask = (1u << nb) - 1u;
+        const int hb = pass & 1;
+        TOPK_TRACE(2 + min(pass, 3));
+        for (int i = tid; i < kTopkWarps * 256; i += kTopkThreads) (&whist[0][0])[i] = 0;
+        __syncthreads();
+        const uint32_t prefix = s_prefix;
+        for (int64_t j = w0 + lane; j < w1; j += 32) {
+            const uint32_t o = keys[j];
+            if ((o & mask) == prefix) atomicAdd(&whist[warp][(o >> shift) & dmask], 1u);
+        }
+        __syncthreads();
+        for (int i = tid; i < 256; i += kTopkThreads) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int w = 0; w < kTopkWarps; ++w) acc += whist[w][i];
+            chist[hb][i] = acc;
+        }
+        cluster_sync_all();  // every CTA's chist[hb] is final (and the peers' previous pass reads are done)
+        // thread = bin: its per-CTA counts (CS distributed-smem loads in flight) and the total
+        uint32_t vr[CS];
+        uint32_t vtot = 0;
+        if (tid < 256) {
+#pragma unroll
+            for (int r = 0; r < CS; ++r) {
+                vr[r] = dsmem_ld(&chist[hb][tid], (uint32_t)r);
+                vtot += vr[r];
+            }
+            tot_bins[tid] = vtot;
+        }
+        __syncthreads();
+        if (tid < 32) {
+            // lane l owns descending digits d = 8l..8l+7 (bin = 255 - d), summed over the cluster
+            uint32_t cnt[8], tot = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                cnt[i] = tot_bins[255 - (8 * tid + i)];
+                tot += cnt[i];
+            }
+            uint32_t incl = tot;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (tid >= o) incl += t;
+            }
+            uint32_t run = incl - tot;
+            const uint32_t need = s_kleft;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (run < need && run + cnt[i] >= need) {
+                    s_sel = (uint32_t)(255 - (8 * tid + i));
+                    s_kleft = need - run;
+                }
+                run += cnt[i];
+            }
+        }
+        __syncthreads();
+        const uint32_t sel = s_sel;
+        // counts of this pass's digits above the selected one (strictly greater than the final
+        // threshold), per CTA and per warp of this CTA; the selected bin's counts are the ties
+        // once the last pass has run
+        if (tid < 256) {  // warps 0..7 cover the 256 bins: per-CTA sums by warp reduction
+            const bool above = (uint32_t)tid > sel && (uint32_t)tid <= dmask;
+#pragma unroll
+            for (int r = 0; r < CS; ++r) {
+                const uint32_t g = __reduce_add_sync(0xffffffffu, above ? vr[r] : 0u);
+                if (lane == 0 && g) atomicAdd(&cta_gt[r], g);
+            }
+        }
+        {   // each warp sums its own histogram's bins above the selected digit
+            uint32_t g = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t d = (uint32_t)(lane * 8 + i);
+                if (d > sel && d <= dmask) g += whist[warp][d];
+            }
+            g = __reduce_add_sync(0xffffffffu, g);
+            if (lane == 0) warp_gt[warp] += g;
+        }
+        if ((uint32_t)tid == sel) {
+#pragma unroll
+            for (int r = 0; r < CS; ++r) cta_eq[r] = vr[r];
+        }
+        if (tid < kTopkWarps) warp_eq[tid] = whist[tid][sel];
+        if (tid == 0) s_prefix = prefix | (sel << shift);
+        mask |= dmask << shift;
+        __syncthreads();
+    }
+    if (lead >= 32) {  // every key equal: all ties
+        if (tid < CS) { cta_gt[tid] = 0; cta_eq[tid] = (uint32_t)max((int64_t)0, min(m, (int64_t)(tid + 1) * seg) - (int64_t)tid * seg); }
+        if (tid < kTopkWarps) { warp_gt[tid] = 0; warp_eq[tid] = (uint32_t)(min(nloc, (tid + 1) * wseg) - min(nloc, tid * wseg)); }
+        __syncthreads();
+    }
+    TOPK_TRACE(6);
+    const uint32_t T = s_prefix;
+    const uint32_t need_eq = s_kleft;
+    const uint32_t G = (uint32_t)k - need_eq;
+    // offsets: CTAs before this one, then warps before this one (index order)
+    uint32_t gt_off = 0, eq_off = 0;
+    for (uint32_t r = 0; r < rank; ++r) { gt_off += cta_gt[r]; eq_off += cta_eq[r]; }
+    for (int w = 0; w < warp; ++w) { gt_off += warp_gt[w]; eq_off += warp_eq[w]; }
+    int32_t* dst = idx_out + row * k;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int64_t j0 = w0; j0 < w1; j0 += 32) {
+        const int64_t j = j0 + lane;
+        const uint32_t o = j < w1 ? keys[j] : 0u;
+        const bool gt = j < w1 && o > T, eq = j < w1 && o == T;
+        const uint32_t gb = __ballot_sync(0xffffffffu, gt);
+        if (gt) dst[gt_off + __popc(gb & lt_mask)] = (int32_t)(c0 + j);
+        gt_off += __popc(gb);
+        const uint32_t eb = __ballot_sync(0xffffffffu, eq);
+        const uint32_t r = eq_off + __popc(eb & lt_mask);
+        if (eq && r < need_eq) dst[G + r] = (int32_t)(c0 + j);
+        eq_off += __popc(eb);
+    }
+    if (rank == 0 && tid == 0 && counts) counts[row] = (int32_t)k;
+    TOPK_TRACE(7);
+    cluster_sync_all();  // peers may still read this CTA's histograms / reductions
+}
+
 // Fallback for k beyond the shared-memory sort: composites staged in global
 // memory, output position = number of selected composites larger than it.
 __global__ void k_topk_collect_global(const float* __restrict__ scores, int64_t m, int64_t k,
@@ -296,6 +499,17 @@ cudaError_t topk_rows(const float* scores, int64_t rows, int64_t m, int64_t k, i
                       int32_t* counts, cudaStream_t s, bool sorted) {
     if (rows == 0) return cudaSuccess;
     if (k > kTopkMaxSortK) return cudaErrorNotSupported;  // caller uses topk_rows_global
+    if (!sorted && rows * 4 <= 148 && m >= 4 * kTopkThreads && (m + 3) / 4 * 4 <= 48 * 1024) {
+        // few long rows: a cluster of 4 CTAs per row (unsorted index set)
+        const size_t csm = sizeof(uint32_t) * (size_t)((m + 3) / 4);
+        static bool cattr = false;
+        if (!cattr) {
+            cudaFuncSetAttribute(k_topk_cluster<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 196 * 1024);
+            cattr = true;
+        }
+        k_topk_cluster<4><<<(unsigned)(rows * 4), kTopkThreads, csm, s>>>(scores, m, k, idx, counts);
+        return cudaGetLastError();
+    }
     int p2 = 64;  // the register runs of the bitonic sort work on 64-element segments
     while (p2 < k) p2 <<= 1;
     const int stage = m <= kTopkMaxSmemRow ? 1 : 0;

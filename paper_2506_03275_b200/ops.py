@@ -68,6 +68,10 @@ class Context:
         """PROD-mode per-call index-set validation (CHECK mode always validates)."""
         raise_for(self.lib, self.lib.csd_ctx_set_validation(self.h, int(bool(enabled))))
 
+    def set_sorted_topk(self, sorted_: bool):
+        """select_top_k order: descending (reference) or the same set in index order."""
+        raise_for(self.lib, self.lib.csd_ctx_set_sorted_topk(self.h, int(bool(sorted_))))
+
     @property
     def launches(self) -> int:
         return int(self.lib.csd_ctx_launch_count(self.h))

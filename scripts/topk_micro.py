@@ -28,7 +28,9 @@ def main():
             fn.argtypes = [ctypes.c_void_p]
             buf = torch.zeros(8, dtype=torch.int64, device="cuda")
             fn(buf.data_ptr())
+            ops.context().set_sorted_topk(False)
             ops.select_top_k(s, k, chunk)
+            ops.context().set_sorted_topk(True)
             torch.cuda.synchronize()
             fn(None)
             t = buf.cpu().tolist()

@@ -98,6 +98,32 @@ def test_topk_large_k_global_path(ops, port):
     assert np.array_equal(N(got.indices).astype(np.int32).reshape(2, 17000), port.select_top_k(s, 17000))
 
 
+@pytest.mark.parametrize("rows,m,k,ties", [(24, 12288, 860, False), (24, 12288, 860, True),
+                                           (8, 4096, 300, True), (3, 20000, 5000, False)])
+def test_topk_unsorted_set_exact(ops, port, rows, m, k, ties):
+    """PROD selection order (csd_ctx_set_sorted_topk(0)): the same exact index set as the
+    reference, strictly-greater entries then the lowest-index ties, each in index order
+    (cluster-of-CTAs path for few long rows)."""
+    rng = np.random.default_rng(rows * m + k)
+    s = rng.random((1, 1, rows, m), dtype=np.float32) * 3 + 1
+    if ties:
+        s = np.round(s * 8) / 8  # many equal scores: the tie rule decides membership
+    want = port.select_top_k(s, k).reshape(rows, k)
+    ctx = ops.context()
+    ctx.set_sorted_topk(False)
+    try:
+        got = N(ops.select_top_k(T(s), k, 1).indices).astype(np.int64).reshape(rows, k)
+    finally:
+        ctx.set_sorted_topk(True)
+    flat = s.reshape(rows, m)
+    for r in range(rows):
+        assert set(got[r].tolist()) == set(want[r].tolist()), r
+        thr = flat[r, want[r][-1]]
+        gt = [i for i in got[r] if flat[r, i] > thr]
+        assert gt == sorted(gt) and list(got[r][:len(gt)]) == gt  # greater first, index order
+        assert list(got[r][len(gt):]) == sorted(got[r][len(gt):].tolist())
+
+
 def test_topk_value_error(ops):
     from paper_2506_03275_b200 import errors
     with pytest.raises(errors.ValueError):
