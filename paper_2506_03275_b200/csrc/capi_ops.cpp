@@ -304,6 +304,16 @@ csd_status csd_mlp_change_indices(csd_ctx* ctx, csd_mode mode, const void* x, co
             return set_error(CSD_ERR_UNSUPPORTED, "production tile means need D %% 64 == 0 and F %% 128 == 0");
         void* ws = c->ws(csd::kWsMeans, prod_means_ws_bytes(batch, n, d, f, chunk));
         CSD_TRY(need_ws(ws));
+        if (!c->sorted_topk && topk_cluster_eligible(rows, f) && k <= f) {
+            // unsorted selection: |T - T_m| reduced inside the cluster top-k's load
+            MeansPartials mp{};
+            CSD_CU(prod_tile_means_tc(x, w1, batch, n, d, f, chunk, tile_means, scores, ws, s, &mp),
+                   "tile_means");
+            CSD_CU(topk_rows_fused_absdiff(mp.partial, mp.ks, tile_means, rows, f, k, idx, counts, s),
+                   "topk_fused");
+            c->launches += 3;
+            return CSD_OK;
+        }
         // |tile_means(x) - T_m| fused into the split-K reduction (mlp.cpp:116)
         CSD_CU(prod_tile_means_tc(x, w1, batch, n, d, f, chunk, tile_means, scores, ws, s),
                "tile_means");

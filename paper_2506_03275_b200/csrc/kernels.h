@@ -54,6 +54,10 @@ cudaError_t check_sparse_delta_mlp(const float* x, const float* w1, const float*
 cudaError_t topk_rows(const float* scores, int64_t rows, int64_t m, int64_t k, int32_t* idx,
                       int32_t* counts, cudaStream_t s, bool sorted = true);
 int64_t topk_max_k();
+bool topk_cluster_eligible(int64_t rows, int64_t m);
+cudaError_t topk_rows_fused_absdiff(const float* partial, int ks, const float* cached, int64_t rows,
+                                    int64_t m, int64_t k, int32_t* idx, int32_t* counts,
+                                    cudaStream_t s);
 cudaError_t topk_rows_global(const float* scores, int64_t rows, int64_t m, int64_t k,
                              int32_t* idx, int32_t* counts, uint64_t* ws, cudaStream_t s);
 cudaError_t validate_index_set(const int32_t* idx, const int32_t* counts, int64_t rows,
@@ -101,9 +105,16 @@ cudaError_t prod_cast_bf16_f32(const void* in, float* out, int64_t n, cudaStream
 // means_tc.cu: tcgen05 tile means (T, or |T - cached| when cached != null)
 bool means_tc_supported(int64_t d, int64_t f);
 size_t prod_means_ws_bytes(int64_t batch, int64_t n, int64_t d, int64_t f, int64_t chunk);
+// With partials_out the split-K partials are left in ws (not reduced into out) and
+// described there, for a consumer that fuses the reduction.
+struct MeansPartials {
+    const float* partial;
+    int ks;
+};
 cudaError_t prod_tile_means_tc(const void* x, const void* w1, int64_t batch, int64_t n,
                                int64_t d, int64_t f, int64_t chunk, const float* cached,
-                               float* out, void* ws, cudaStream_t s);
+                               float* out, void* ws, cudaStream_t s,
+                               MeansPartials* partials_out = nullptr);
 // dense-step MLP epilogue: act = gelu(pre + b1) row-major + chunk-major cache copy
 cudaError_t prod_bias_gelu_cm(const void* pre, const float* b1, int64_t batch, int64_t n,
                               int64_t f, int64_t chunk, void* act, void* cm, cudaStream_t s);

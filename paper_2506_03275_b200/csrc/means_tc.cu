@@ -52,7 +52,7 @@ k_chunk_means_split(const __nv_bfloat16* __restrict__ x, int64_t n, int64_t d, i
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (col0 < d) {
         const __nv_bfloat16* src = x + (b * n + c * chunk) * d + col0;
-#pragma unroll 4
+#pragma unroll 12
         for (int64_t r = warp; r < chunk; r += 8) {
             const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + r * d));
             const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
@@ -197,7 +197,7 @@ static int pick_ksplit(int64_t /*tiles*/, int64_t kblocks) { return kblocks % 2 
 // ws: bop [ntiles*128, D] bf16 + partials [ksplit][BC][F] fp32 (see prod_means_ws_bytes).
 cudaError_t prod_tile_means_tc(const void* x, const void* w1, int64_t batch, int64_t n,
                                int64_t d, int64_t f, int64_t chunk, const float* cached,
-                               float* out, void* ws, cudaStream_t s) {
+                               float* out, void* ws, cudaStream_t s, MeansPartials* partials_out) {
     if (d % 64 || f % 128) return cudaErrorNotSupported;
     const int64_t bc = batch * (n / chunk);
     const int64_t ntiles = (bc + 63) / 64;
@@ -221,6 +221,11 @@ cudaError_t prod_tile_means_tc(const void* x, const void* w1, int64_t batch, int
     }
     k_tile_means_tc<<<dim3((unsigned)mtiles, (unsigned)ntiles, (unsigned)ks), 128, smem, s>>>(tw, tb, p);
     const int64_t total = bc * f;
+    if (partials_out != nullptr) {  // the caller fuses the reduction (top-k load)
+        partials_out->partial = partial;
+        partials_out->ks = ks;
+        return cudaGetLastError();
+    }
     k_means_reduce<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(partial, ks, total, cached, out);
     return cudaGetLastError();
 }

@@ -291,10 +291,18 @@ __device__ __forceinline__ uint32_t cluster_rank() {
     return r;
 }
 
-template <int CS>
+// Fused MLP selection scores (mlp.cpp:116): score = |sum_s partial[s] - cached| in the same
+// fixed summation order as k_means_reduce, so the keys are bit-identical to the unfused path.
+struct TopkFusedScores {
+    const float* partial;  // [ks][rows * m]
+    int ks;
+    const float* cached;   // [rows * m]
+};
+
+template <int CS, bool kFused>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kTopkThreads)
 k_topk_cluster(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* __restrict__ idx_out,
-               int32_t* __restrict__ counts) {
+               int32_t* __restrict__ counts, TopkFusedScores fs) {
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t* keys = reinterpret_cast<uint32_t*>(smem);  // this CTA's segment
     __shared__ uint32_t whist[kTopkWarps][256];
@@ -315,7 +323,16 @@ k_topk_cluster(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* 
     const int64_t w0 = min(nloc, warp * wseg), w1 = min(nloc, w0 + wseg);
     uint32_t kand = 0xffffffffu, kor = 0u;
     for (int64_t j = w0 + lane; j < w1; j += 32) {
-        const uint32_t o = ord_key(src[c0 + j]);
+        float sc;
+        if constexpr (kFused) {
+            const int64_t e = row * m + c0 + j, total = (int64_t)gridDim.x / CS * m;
+            float acc = fs.partial[e];
+            for (int q = 1; q < fs.ks; ++q) acc += fs.partial[(int64_t)q * total + e];
+            sc = fabsf(acc - fs.cached[e]);
+        } else {
+            sc = src[c0 + j];
+        }
+        const uint32_t o = ord_key(sc);
         keys[j] = o;
         kand &= o;
         kor |= o;
@@ -495,19 +512,41 @@ __global__ void k_topk_emit_global(const uint64_t* ws, int64_t rows, int64_t k, 
 
 int64_t topk_max_k() { return kTopkMaxSortK; }
 
+bool topk_cluster_eligible(int64_t rows, int64_t m) {
+    return rows * 4 <= 148 && m >= 4 * kTopkThreads && (m + 3) / 4 * 4 <= 48 * 1024;
+}
+
+// Unsorted top-k of |sum_s partial[s] - cached| (the MLP change scores) without materialising
+// the scores: the split-K reduction of the tile means runs inside the top-k load.
+cudaError_t topk_rows_fused_absdiff(const float* partial, int ks, const float* cached, int64_t rows,
+                                    int64_t m, int64_t k, int32_t* idx, int32_t* counts,
+                                    cudaStream_t s) {
+    if (!topk_cluster_eligible(rows, m)) return cudaErrorNotSupported;
+    const size_t csm = sizeof(uint32_t) * (size_t)((m + 3) / 4);
+    static bool cattr = false;
+    if (!cattr) {
+        cudaFuncSetAttribute(k_topk_cluster<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 196 * 1024);
+        cattr = true;
+    }
+    k_topk_cluster<4, true><<<(unsigned)(rows * 4), kTopkThreads, csm, s>>>(
+        nullptr, m, k, idx, counts, TopkFusedScores{partial, ks, cached});
+    return cudaGetLastError();
+}
+
 cudaError_t topk_rows(const float* scores, int64_t rows, int64_t m, int64_t k, int32_t* idx,
                       int32_t* counts, cudaStream_t s, bool sorted) {
     if (rows == 0) return cudaSuccess;
     if (k > kTopkMaxSortK) return cudaErrorNotSupported;  // caller uses topk_rows_global
-    if (!sorted && rows * 4 <= 148 && m >= 4 * kTopkThreads && (m + 3) / 4 * 4 <= 48 * 1024) {
+    if (!sorted && topk_cluster_eligible(rows, m)) {
         // few long rows: a cluster of 4 CTAs per row (unsorted index set)
         const size_t csm = sizeof(uint32_t) * (size_t)((m + 3) / 4);
         static bool cattr = false;
         if (!cattr) {
-            cudaFuncSetAttribute(k_topk_cluster<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 196 * 1024);
+            cudaFuncSetAttribute(k_topk_cluster<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 196 * 1024);
             cattr = true;
         }
-        k_topk_cluster<4><<<(unsigned)(rows * 4), kTopkThreads, csm, s>>>(scores, m, k, idx, counts);
+        k_topk_cluster<4, false><<<(unsigned)(rows * 4), kTopkThreads, csm, s>>>(scores, m, k, idx, counts,
+                                                                                  TopkFusedScores{});
         return cudaGetLastError();
     }
     int p2 = 64;  // the register runs of the bitonic sort work on 64-element segments

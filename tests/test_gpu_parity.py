@@ -369,3 +369,23 @@ def test_prod_block_cfg1_vs_check_mode(ops, port):
         yc = chk.step(T(x), bool(dense))
         err = rel_l2(N(yp) - x, N(yc) - x)  # branch outputs (x cancels)
         assert err < REL_L2_TOL, (t, err)
+
+
+def test_prod_mlp_change_indices_fused_unsorted_same_set(ops, port):
+    """The PROD block's fused selection (split-K tile-means reduction inside the cluster
+    top-k, unsorted) yields the same index sets as the sorted public path."""
+    b, n, d, f, c, kk = 1, 1536, 512, 4096, 64, 300
+    x = bf(port.gaussian(700, (b, n, d)))
+    w1 = bf(port.gaussian(701, (f, d), 1 / 16))
+    tm = T(port.gaussian(702, (b, n // c, f), 0.1))
+    xt, wt = T(x, torch.bfloat16), T(w1, torch.bfloat16)
+    want = N(ops.mlp_change_indices(xt, wt, tm, kk, c).indices).astype(np.int64)
+    ctx = ops.context()
+    ctx.set_sorted_topk(False)
+    try:
+        got = N(ops.mlp_change_indices(xt, wt, tm, kk, c).indices).astype(np.int64)
+    finally:
+        ctx.set_sorted_topk(True)
+    got, want = got.reshape(-1, kk), want.reshape(-1, kk)
+    for r in range(got.shape[0]):
+        assert set(got[r].tolist()) == set(want[r].tolist()), r
