@@ -8,10 +8,12 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "tc_common.cuh"
 #include "kernels.h"
 
 namespace csd {
 namespace dev {
+using csd::tc::pack_bf16x2;
 
 __global__ void k_cast_f32_bf16(const float* in, __nv_bfloat16* out, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -50,35 +52,56 @@ __global__ void __launch_bounds__(256)
 k_bias_gelu_cm(const __nv_bfloat16* __restrict__ pre, const float* __restrict__ b1, int64_t n,
                int64_t f, int64_t chunk, __nv_bfloat16* __restrict__ act,
                __nv_bfloat16* __restrict__ cm) {
-    __shared__ __nv_bfloat16 tile[64][66];
+    // 16-byte accesses in both passes: row pass = 8 columns per thread-step, chunk-major
+    // pass = 8 consecutive rows of one column per thread-step (tile pitch 72 bf16: the
+    // column reads of the second pass hit distinct banks)
+    __shared__ __align__(16) __nv_bfloat16 tile[64][72];
     const int64_t z = blockIdx.z;  // b * C + c
     const int64_t nc = n / chunk;
     const int64_t b = z / nc, c = z % nc;
     const int64_t r0 = (int64_t)blockIdx.y * 64, f0 = (int64_t)blockIdx.x * 64;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-    // row-major pass: each thread 2 columns, rows ty, ty+8, ...
-    for (int rr = ty; rr < 64; rr += 8) {
+    const int tid = threadIdx.x;
+    const int cg = tid & 7;  // 8-column group
+    float bias[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) bias[u] = b1[f0 + cg * 8 + u];
+#pragma unroll
+    for (int rep = 0; rep < 2; ++rep) {
+        const int rr = (tid >> 3) + rep * 32;
         const int64_t r = r0 + rr;
-        if (r >= chunk) break;
+        if (r >= chunk) continue;
         const int64_t row = b * n + c * chunk + r;
-        const int64_t col = f0 + 2 * tx;
-        if (col + 1 < f + 1) {
-            const __nv_bfloat162 p2 = *reinterpret_cast<const __nv_bfloat162*>(pre + row * f + col);
-            const float2 pf = __bfloat1622float2(p2);
-            const __nv_bfloat162 a2 =
-                __floats2bfloat162_rn(fast_gelu(pf.x + b1[col]), fast_gelu(pf.y + b1[col + 1]));
-            *reinterpret_cast<__nv_bfloat162*>(act + row * f + col) = a2;
-            tile[rr][2 * tx] = a2.x;
-            tile[rr][2 * tx + 1] = a2.y;
+        const uint4 pv = *reinterpret_cast<const uint4*>(pre + row * f + f0 + cg * 8);
+        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&pv);
+        uint32_t o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float2 pf = __bfloat1622float2(p2[u]);
+            o[u] = pack_bf16x2(gelu_tanh_approx(pf.x + bias[2 * u]), gelu_tanh_approx(pf.y + bias[2 * u + 1]));
         }
+        const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(act + row * f + f0 + cg * 8) = ov;
+        *reinterpret_cast<uint4*>(&tile[rr][cg * 8]) = ov;
     }
     __syncthreads();
-    // chunk-major pass: cm[z][f0 + j][r0 + i], contiguous along i
-    for (int jj = ty; jj < 64; jj += 8) {
-        const int64_t col = f0 + jj;
-        __nv_bfloat16* dst = cm + (z * f + col) * chunk + r0;
-        for (int i = tx; i < 64; i += 32)
-            if (r0 + i < chunk) dst[i] = tile[i][jj];
+    // chunk-major pass: cm[z][f0 + j][r0 + 8 g .. + 7]
+#pragma unroll
+    for (int rep = 0; rep < 2; ++rep) {
+        const int jj = (tid >> 3) + rep * 32, g8 = tid & 7;
+        const int64_t rbase = r0 + g8 * 8;
+        if (rbase >= chunk) continue;
+        uint32_t w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const __nv_bfloat16 lo = tile[g8 * 8 + 2 * u][jj], hi = tile[g8 * 8 + 2 * u + 1][jj];
+            w[u] = (uint32_t)__bfloat16_as_ushort(lo) | ((uint32_t)__bfloat16_as_ushort(hi) << 16);
+        }
+        __nv_bfloat16* dst = cm + (z * f + f0 + jj) * chunk + rbase;
+        if (rbase + 8 <= chunk) {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+            for (int i = 0; i < (int)(chunk - rbase); ++i) dst[i] = tile[g8 * 8 + i][jj];
+        }
     }
 }
 __global__ void k_cm_to_ref(const __nv_bfloat16* cm, int64_t n, int64_t f, int64_t chunk,
@@ -127,7 +150,7 @@ __global__ void k_bias_add_rows(float* __restrict__ out, const float* __restrict
 
 cudaError_t prod_bias_gelu_cm(const void* pre, const float* b1, int64_t batch, int64_t n,
                               int64_t f, int64_t chunk, void* act, void* cm, cudaStream_t s) {
-    if (f % 64) return cudaErrorNotSupported;
+    if (f % 64 || chunk % 8) return cudaErrorNotSupported;  // 16-byte chunk-major rows
     dim3 g((unsigned)(f / 64), (unsigned)((chunk + 63) / 64), (unsigned)(batch * (n / chunk)));
     k_bias_gelu_cm<<<g, 256, 0, s>>>((const __nv_bfloat16*)pre, b1, n, f, chunk,
                                      (__nv_bfloat16*)act, (__nv_bfloat16*)cm);
