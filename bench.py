@@ -271,6 +271,7 @@ def run_ours(args, rank, world):
 
     # ---- kernel micro-benchmarks: column-sparse vs same-family dense attention
     kern = attention_kernel_bench(ops, torch, cfg, n, attn_k, args.kernel_reps)
+    mlp_kern = mlp_kernel_bench(ops, torch, cfg, n, mlp_k, args.kernel_reps)
 
     out = None
     if rank == 0:
@@ -303,6 +304,7 @@ def run_ours(args, rank, world):
             "dense_step_ms": round(statistics.median(dense_ms), 4) if dense_ms else None,
             "sparse_step_ms": round(statistics.median(sparse_ms), 4) if sparse_ms else None,
             "attention": kern,
+            "mlp": mlp_kern,
             "clocks": clocks,
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms/step", "h2d_bytes_per_step": io_bytes,
                     "d2h_bytes_per_step": io_bytes,
@@ -337,7 +339,7 @@ def profiled_traffic(kernel_substr):
         return None
 
 
-def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps):
+def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps, dense_ms=None):
     """Sparse (k = attn_k) vs dense (all N keys, same kernel family) attention on the FLUX
     shape, inputs resident in HBM, L2 flushed between repetitions."""
     h, e, c = cfg["heads"], cfg["head_dim"], cfg["chunk"]
@@ -379,7 +381,7 @@ def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps):
     ops.context().set_validation(False)  # the index set comes from top-k: valid by construction
     t_sparse = timed(lambda: ops.sparse_delta_attention(q, k, v, idx, base, 1.0, layout=1, out=out))
     ops.context().set_validation(True)
-    t_dense = timed(lambda: ops.dense_attention(q, k, v, layout=1))
+    t_dense = dense_ms if dense_ms is not None else timed(lambda: ops.dense_attention(q, k, v, layout=1))
     elem = 2
     alg_bytes = 5 * n * h * e * elem  # Q, K, V, base, out
     flops = 4.0 * h * n * attn_k * e  # flops.cpp:40-43
@@ -391,6 +393,57 @@ def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps):
                       "tflops": round(dense_flops / (t_dense * 1e-3) / 1e12, 2)},
             "speedup_vs_dense": round(t_dense / t_sparse, 3),
             "k": attn_k, "n": n, "reps": reps, "l2_flush": "256 MB write between reps"}
+
+
+def mlp_kernel_bench(ops, torch, cfg, n, mlp_k, reps):
+    """Sparse-delta MLP (up + down, csd_sparse_delta_mlp) on the FLUX shape with k = mlp_k
+    selected neurons per chunk, against the dense MLP (csd_dense_mlp); inputs resident in HBM,
+    L2 flushed between repetitions."""
+    d, f, c = cfg["dim"], cfg["hidden"], cfg["chunk"]
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn((1, n, d), device="cuda", generator=g).to(torch.bfloat16)
+    w = ops.MlpWeights((torch.randn((f, d), device="cuda", generator=g) / d ** 0.5).to(torch.bfloat16),
+                       torch.randn((f,), device="cuda", generator=g) / d ** 0.5,
+                       (torch.randn((f, d), device="cuda", generator=g) / d ** 0.5 / 2).to(torch.bfloat16),
+                       torch.randn((d,), device="cuda", generator=g) / d ** 0.5 / 2)
+    cache = ops.MlpCache()
+    ops.mlp_step(x, w, cache, True, mlp_k, c)  # dense step: caches + tile means
+    idx = ops.mlp_change_indices(x, w.w1, cache.tile_means, mlp_k, c)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def timed(fn):
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            fn()
+        stream.wait_stream(side)
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            fn()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(reps + 3)]
+        for i, (a, b) in enumerate(evs):
+            flush.fill_(float(i))
+            a.record(stream)
+            gr.replay()
+            b.record(stream)
+        torch.cuda.synchronize()
+        return statistics.median(a.elapsed_time(b) for a, b in evs[3:])
+
+    ops.context().set_validation(False)
+    t_sparse = timed(lambda: ops.sparse_delta_mlp(x, w, idx, cache))
+    ops.context().set_validation(True)
+    t_dense = timed(lambda: ops.dense_mlp(x, w, c))
+    flops = 4.0 * n * d * mlp_k          # flops.cpp:50 (up + down over the selected neurons)
+    dense_flops = 4.0 * n * d * f
+    return {"sparse": {"ms": round(t_sparse, 5), "flops": flops,
+                       "eff_tflops": round(flops / (t_sparse * 1e-3) / 1e12, 2),
+                       "dense_equiv_tflops": round(dense_flops / (t_sparse * 1e-3) / 1e12, 2)},
+            "dense": {"ms": round(t_dense, 5), "flops": dense_flops,
+                      "tflops": round(dense_flops / (t_dense * 1e-3) / 1e12, 2)},
+            "speedup_vs_dense": round(t_dense / t_sparse, 3), "k": mlp_k, "reps": reps,
+            "l2_flush": "256 MB write between reps"}
 
 
 # ---------------------------------------------------------------------------- reference arm
