@@ -322,6 +322,12 @@ def run_ours(args, rank, world):
                                 "profiles/latest_full.json)",
                 "alg_bytes": att["alg_bytes"],
                 "tensor_frac": round(att["flops"] / (att["ms"] * 1e-3) / 1e12 / tf, 4),
+                # the binding staging path: gathered K/V row pieces through TMA tile::gather4,
+                # whose per-SM rate (14 B/ns, scripts/gather_bench2.cu) caps the kernel
+                "gather": {"bytes": att["gather_bytes"],
+                           "achieved_gbs": round(att["gather_bytes"] / (att["ms"] * 1e-3) / 1e9, 1),
+                           "measured_gather4_gbs": 148 * 14.0,
+                           "frac": round(att["gather_bytes"] / (att["ms"] * 1e-3) / 1e9 / (148 * 14.0), 4)},
             },
         }
     return out
@@ -384,9 +390,11 @@ def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps, dense_ms=None):
     t_dense = dense_ms if dense_ms is not None else timed(lambda: ops.dense_attention(q, k, v, layout=1))
     elem = 2
     alg_bytes = 5 * n * h * e * elem  # Q, K, V, base, out
+    gather_bytes = 2 * h * (n // c) * (((attn_k + 3) // 4) * 4) * e * elem  # K + V rows, 4-row groups
     flops = 4.0 * h * n * attn_k * e  # flops.cpp:40-43
     dense_flops = 4.0 * h * n * n * e  # flops.cpp:35-38
-    return {"sparse": {"ms": round(t_sparse, 5), "alg_bytes": alg_bytes, "flops": flops,
+    return {"sparse": {"ms": round(t_sparse, 5), "alg_bytes": alg_bytes, "gather_bytes": gather_bytes,
+                       "flops": flops,
                        "eff_tflops": round(flops / (t_sparse * 1e-3) / 1e12, 2),
                        "dense_equiv_tflops": round(dense_flops / (t_sparse * 1e-3) / 1e12, 2)},
             "dense": {"ms": round(t_dense, 5), "flops": dense_flops,

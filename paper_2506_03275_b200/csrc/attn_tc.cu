@@ -152,8 +152,11 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     uint8_t* const sk = smem + p.off_k;
     uint8_t* const sv = smem + p.off_v;
     // copy_mode 2: odd CTAs copy (LSU), even CTAs gather (TMA) -- TPC siblings split the paths
-    const bool cpm = !dense && (p.copy_mode == 1 || (p.copy_mode == 2 && (blockIdx.x & 1)));
+    const bool cpm = !dense && (p.copy_mode == 1 || p.copy_mode == 3 || (p.copy_mode == 2 && (blockIdx.x & 1)));
     const int sm_threads = cpm ? p.sm_threads_copy : p.sm_threads;
+    // copy_mode 3 (split): K by TMA gather4 from the producer warps, V by cp.async from the
+    // idle softmax warps -- the two staging paths run concurrently
+    const bool split = cpm && p.copy_mode == 3;
 
     if (cpm) {
         // partial key blocks copy only their live rows; the stale V rows they leave behind
@@ -166,9 +169,9 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         mbar_init(bar_q, 1);
         for (int i = 0; i < 2; ++i) {
             // copy mode: one cp.async-tracking arrival per copy thread
-            mbar_init(bar_kf + i, cpm ? p.ncopy : 1);
+            mbar_init(bar_kf + i, (cpm && !split) ? p.ncopy : 1);
             mbar_init(bar_ke + i, 1);
-            mbar_init(bar_vf + i, cpm ? p.ncopy : 1);
+            mbar_init(bar_vf + i, cpm ? (split ? p.ncopy - 96 : p.ncopy) : 1);
             mbar_init(bar_ve + i, 1);
             mbar_init(bar_ids + i, 1);
         }
@@ -278,7 +281,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 const int s = gb & 1;
                 const int nvalid = min(128, cnt - j * 128);
                 int32_t rows[4] = {0, 0, 0, 0};
-                if (!dense && (warp == 0 || (!cpm && warp <= 3))) {
+                if (!dense && (warp == 0 || ((!cpm || split) && warp <= 3))) {
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         int r = j * 128 + lane * 4 + i;
@@ -296,11 +299,25 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                         __syncwarp();
                         if (lane == 0) mbar_arrive(bar_ids + s);
                     }
-                    mbar_wait(bar_ids + s, (gb >> 1) & 1);
                     if (warp == 0 && lane == 0) ATTN_TRACE(16 + gb);
+                    if (split && warp <= 3) {
+                        // split mode: K rows by TMA gather4 (live 4-row groups, warps 0/2/3);
+                        // the idle softmax warps copy V with cp.async at the same time
+                        const int ngroups = (nvalid + 3) >> 2;
+                        if (warp == 0 && lane == 0)
+                            mbar_arrive_expect_tx(bar_kf + s, (uint32_t)ngroups * 4u * (uint32_t)E * 2u);
+                        if ((lane % 3) == pw && lane < ngroups)
+                            for (int hf = 0; hf < L::kHalves; ++hf)
+                                tma_gather4(&tm_kg, bar_kf + s, sk + s * L::kKV + hf * L::kStrip + lane * 512,
+                                            col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
+                        if (warp == 0 && lane == 0) ATTN_TRACE(48 + gb);
+                        continue;
+                    }
+                    mbar_wait(bar_ids + s, (gb >> 1) & 1);
                     const int32_t* tab = ids_tab + s * 128;
+                    const int c0 = split ? ct - 96 : ct, cstride = split ? p.ncopy - 96 : p.ncopy;
                     auto copy_rows = [&](const __nv_bfloat16* src_t, uint8_t* dst) {
-                        for (int idx = ct; idx < nvalid * kPieces; idx += p.ncopy) {
+                        for (int idx = c0; idx < nvalid * kPieces; idx += cstride) {
                             const int r = idx / kPieces, piece = idx - r * kPieces;
                             const char* src = reinterpret_cast<const char*>(
                                 src_t + (int64_t)tab[r] * p.pitch + col0) + piece * 16;
@@ -309,8 +326,10 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
                         }
                     };
-                    copy_rows(p.k, sk + s * L::kKV);
-                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar_kf + s)) : "memory");
+                    if (!split) {
+                        copy_rows(p.k, sk + s * L::kKV);
+                        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar_kf + s)) : "memory");
+                    }
                     copy_rows(p.v, sv + s * L::kKV);
                     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar_vf + s)) : "memory");
                     if (warp == 0 && lane == 0) ATTN_TRACE(48 + gb);
