@@ -389,3 +389,28 @@ def test_prod_mlp_change_indices_fused_unsorted_same_set(ops, port):
     got, want = got.reshape(-1, kk), want.reshape(-1, kk)
     for r in range(got.shape[0]):
         assert set(got[r].tolist()) == set(want[r].tolist()), r
+
+
+def test_prod_block_batch2_vs_check_mode(ops, port):
+    """Batch 2 through the PROD block step (every kernel's batch indexing) against CHECK mode
+    on the same bf16-rounded inputs: dense then sparse steps, branch outputs within 2e-2."""
+    b, n, d, h, e, f, c = 2, 512, 256, 2, 128, 1024, 64
+    ak, mk = 52, 103
+    std = 1 / np.sqrt(d)
+    w = {"wq": port.gaussian(11, (d, d), std), "wk": port.gaussian(12, (d, d), std),
+         "wv": port.gaussian(13, (d, d), std), "wo": port.gaussian(14, (d, d), std / 2),
+         "w1": port.gaussian(15, (f, d), std), "b1": port.gaussian(16, (f,), std),
+         "w2": port.gaussian(17, (f, d), std / 2), "b2": port.gaussian(18, (d,), std / 2)}
+    w = {k: bf(v) if k not in ("b1", "b2") else v for k, v in w.items()}
+    cfg = ops.BlockConfig(batch=b, seq=n, dim=d, heads=h, head_dim=e, hidden=f, chunk=c,
+                          attn_k=ak, mlp_k=mk)
+    prod = ops.Block(cfg, w, production=True)
+    chk = ops.Block(cfg, w, production=False)
+    x0 = port.gaussian(2235, (b, n, d))
+    for t, dense in enumerate([1, 0, 0]):
+        x = bf(x0 + 0.02 * t * port.gaussian(4000 + t, x0.shape))
+        yp = prod.step(T(x, torch.bfloat16), bool(dense))
+        yc = chk.step(T(x), bool(dense))
+        for bb in range(b):
+            err = rel_l2(N(yp)[bb] - x[bb], N(yc)[bb] - x[bb])
+            assert err < REL_L2_TOL, (t, bb, err)
