@@ -82,6 +82,26 @@ csd_status gemm_bf16(Ctx* ctx, const void* a, const void* b, bool b_nk, void* c,
     return CSD_OK;
 }
 
+// Per-chunk GEMM over the chunk-major activation cache [B*C, F, chunk] (mlp_tc.cu layout):
+// out[z*chunk + r, :] = sum_f cm[z, f, r] * W2[f, :] for every chunk z, as one strided-
+// batched call (A^T of each chunk is the contiguous [F, chunk] slab; W2 shared).
+csd_status gemm_bf16_chunks(Ctx* ctx, const void* cm, const void* w2, void* out, bool c_f32,
+                            int64_t chunks, int64_t chunk, int64_t d, int64_t f, cudaStream_t s) {
+    cublasHandle_t h = ctx->blas();
+    cublasSetStream(h, s);
+    const float alpha = 1.0f, beta = 0.0f;
+    // column-major per chunk: C^T[D, chunk] = W2^T[D, F] * (act_z)^T[F, chunk], act_z being the
+    // column-major [chunk, F] view of the [F, chunk] slab (ld = chunk, op T)
+    cublasStatus_t st = cublasGemmStridedBatchedEx(
+        h, CUBLAS_OP_N, CUBLAS_OP_T, (int)d, (int)chunk, (int)f, &alpha, w2, CUDA_R_16BF, (int)d,
+        0, cm, CUDA_R_16BF, (int)chunk, f * chunk, &beta, out, c_f32 ? CUDA_R_32F : CUDA_R_16BF,
+        (int)d, chunk * d, (int)chunks, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+    if (st != CUBLAS_STATUS_SUCCESS)
+        return set_error(CSD_ERR_CUDA, "cublasGemmStridedBatchedEx failed (%d)", (int)st);
+    ctx->library_launches += 1;
+    return CSD_OK;
+}
+
 csd_status check_flags(Ctx* ctx, cudaStream_t s) {
     uint32_t f = 0;
     cudaError_t e = cudaMemcpyAsync(&f, ctx->flags, sizeof(f), cudaMemcpyDeviceToHost, s);

@@ -52,6 +52,8 @@ csd_status cuda_status(cudaError_t e, const char* where);
 csd_status check_flags(Ctx* ctx, cudaStream_t s);
 csd_status gemm_bf16(Ctx* ctx, const void* a, const void* b, bool b_nk, void* c, bool c_f32,
                      int64_t m, int64_t n, int64_t k, float beta, cudaStream_t s);
+csd_status gemm_bf16_chunks(Ctx* ctx, const void* cm, const void* w2, void* out, bool c_f32,
+                            int64_t chunks, int64_t chunk, int64_t d, int64_t f, cudaStream_t s);
 csd_status prod_dense_mlp(Ctx* c, const void* x, const void* w1, const float* b1, const void* w2,
                           const float* b2, int64_t batch, int64_t n, int64_t d, int64_t f,
                           int64_t chunk, float* out, void* act_cm, const void* x_mid, void* x_out,

@@ -74,24 +74,34 @@ csd_status prod_attn(Ctx* c, const AttnTcArgs& a, cudaStream_t s) {
 
 namespace csd {
 // Dense MLP, PROD (mlp.cpp:49-81): cuBLAS GEMM1 -> bf16 pre; fused bias+GELU writing the
-// row-major activations and the chunk-major cache; cuBLAS GEMM2 -> fp32 M_cache; fused
+// chunk-major cache (+ row-major activations when chunk > 256); cuBLAS GEMM2 (per chunk over
+// the cache) -> fp32 M_cache; fused
 // +b2 (and, for the block runner, x_out = x_mid + M_cache).
 csd_status prod_dense_mlp(Ctx* c, const void* x, const void* w1, const float* b1, const void* w2,
                           const float* b2, int64_t batch, int64_t n, int64_t d, int64_t f,
                           int64_t chunk, float* out, void* act_cm, const void* x_mid, void* x_out,
                           cudaStream_t s) {
     const int64_t rows = batch * n;
+    // chunk <= 256: GELU writes only the chunk-major cache and GEMM2 runs per chunk over it
+    // (saves the [rows, F] row-major activation write); otherwise the row-major path
+    const bool from_cm = chunk <= 256;
     void* pre = c->ws(kWsPre, 2 * rows * f);
-    void* act = c->ws(kWsAct, 2 * rows * f);
     CSD_TRY(need_ws(pre));
-    CSD_TRY(need_ws(act));
+    void* act = nullptr;
+    if (!from_cm) {
+        act = c->ws(kWsAct, 2 * rows * f);
+        CSD_TRY(need_ws(act));
+    }
     if (!act_cm) {
         act_cm = c->ws(kWsScores, 2 * rows * f);
         CSD_TRY(need_ws(act_cm));
     }
     CSD_TRY(gemm_bf16(c, x, w1, true, pre, false, rows, f, d, 0.0f, s));
     CSD_CU(prod_bias_gelu_cm(pre, b1, batch, n, f, chunk, act, act_cm, s), "bias_gelu_cm");
-    CSD_TRY(gemm_bf16(c, act, w2, false, out, true, rows, d, f, 0.0f, s));
+    if (from_cm)
+        CSD_TRY(gemm_bf16_chunks(c, act_cm, w2, out, true, batch * (n / chunk), chunk, d, f, s));
+    else
+        CSD_TRY(gemm_bf16(c, act, w2, false, out, true, rows, d, f, 0.0f, s));
     CSD_CU(prod_bias_add_rows(out, b2, rows, d, x_mid, x_out, s), "bias_add");
     c->launches += 2;
     return CSD_OK;

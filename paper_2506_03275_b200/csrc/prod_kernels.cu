@@ -104,6 +104,71 @@ k_bias_gelu_cm(const __nv_bfloat16* __restrict__ pre, const float* __restrict__ 
         }
     }
 }
+// Same epilogue, one CTA per (chunk, 64 hidden columns) covering all `chunk` rows: warp w
+// owns 8-column group w, lane l row pairs (2p, 2p+1), p = l + 32 * band.  All loads of the
+// CTA are issued before any math; each row pair's 8 GELU'd columns are packed as words
+// (row 2p | row 2p+1 << 16) into tile_t[col][p], so the chunk-major pass reads 16-byte runs
+// of 8 rows of one column and the CTA's 64 x chunk output block — contiguous in the
+// [B, C, F, chunk] cache — is written as one linear run of 16-byte stores.  `act` may be
+// null: the dense GEMM2 then reads the chunk-major cache directly (prod_dense_mlp).
+template <int kBands>  // ceil(chunk / 64)
+__global__ void __launch_bounds__(256)
+k_bias_gelu_cm_rows(const __nv_bfloat16* __restrict__ pre, const float* __restrict__ b1,
+                    int64_t n, int64_t f, int64_t chunk, __nv_bfloat16* __restrict__ act,
+                    __nv_bfloat16* __restrict__ cm) {
+    extern __shared__ __align__(16) uint32_t tile_t[];  // [64][pw] words
+    const int pw = (int)(chunk / 2) + 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t z = blockIdx.y, nc = n / chunk;
+    const int64_t b = z / nc, c = z % nc;
+    const int64_t f0 = (int64_t)blockIdx.x * 64, col = f0 + warp * 8;
+    const int64_t row0 = b * n + c * chunk;
+    uint4 v[kBands][2];
+#pragma unroll
+    for (int band = 0; band < kBands; ++band) {
+        const int64_t r = 2 * (lane + 32 * band);
+        if (r < chunk) {
+            v[band][0] = __ldg(reinterpret_cast<const uint4*>(pre + (row0 + r) * f + col));
+            v[band][1] = __ldg(reinterpret_cast<const uint4*>(pre + (row0 + r + 1) * f + col));
+        }
+    }
+    float bias[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) bias[u] = b1[col + u];
+#pragma unroll
+    for (int band = 0; band < kBands; ++band) {
+        const int p = lane + 32 * band;
+        const int64_t r = 2 * p;
+        if (r >= chunk) continue;
+        uint32_t o[2][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&v[band][h]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float2 pf = __bfloat1622float2(p2[u]);
+                o[h][u] = pack_bf16x2(gelu_tanh_approx(pf.x + bias[2 * u]),
+                                      gelu_tanh_approx(pf.y + bias[2 * u + 1]));
+            }
+            if (act != nullptr)
+                *reinterpret_cast<uint4*>(act + (row0 + r + h) * f + col) =
+                    make_uint4(o[h][0], o[h][1], o[h][2], o[h][3]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // columns 2u, 2u+1: interleave the two rows
+            tile_t[(warp * 8 + 2 * u) * pw + p] = __byte_perm(o[0][u], o[1][u], 0x5410);
+            tile_t[(warp * 8 + 2 * u + 1) * pw + p] = __byte_perm(o[0][u], o[1][u], 0x7632);
+        }
+    }
+    __syncthreads();
+    const int per_col = (int)(chunk / 8);  // 16-byte pieces per column
+    uint4* dst = reinterpret_cast<uint4*>(cm + (z * f + f0) * chunk);
+    for (int piece = threadIdx.x; piece < 64 * per_col; piece += 256) {
+        const int jj = piece / per_col, q = piece - jj * per_col;
+        dst[piece] = *reinterpret_cast<const uint4*>(tile_t + jj * pw + 4 * q);
+    }
+}
+
 __global__ void k_cm_to_ref(const __nv_bfloat16* cm, int64_t n, int64_t f, int64_t chunk,
                             int64_t total_rows, float* out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -151,6 +216,19 @@ __global__ void k_bias_add_rows(float* __restrict__ out, const float* __restrict
 cudaError_t prod_bias_gelu_cm(const void* pre, const float* b1, int64_t batch, int64_t n,
                               int64_t f, int64_t chunk, void* act, void* cm, cudaStream_t s) {
     if (f % 64 || chunk % 8) return cudaErrorNotSupported;  // 16-byte chunk-major rows
+    if (chunk <= 256) {
+        const dim3 gr((unsigned)(f / 64), (unsigned)(batch * (n / chunk)));
+        const size_t sm = 64 * (size_t)(chunk / 2 + 4) * 4;
+        const auto* pp = (const __nv_bfloat16*)pre;
+        auto* a = (__nv_bfloat16*)act;
+        auto* m = (__nv_bfloat16*)cm;
+        const int bands = (int)((chunk + 63) / 64);
+        if (bands == 1) k_bias_gelu_cm_rows<1><<<gr, 256, sm, s>>>(pp, b1, n, f, chunk, a, m);
+        else if (bands == 2) k_bias_gelu_cm_rows<2><<<gr, 256, sm, s>>>(pp, b1, n, f, chunk, a, m);
+        else if (bands == 3) k_bias_gelu_cm_rows<3><<<gr, 256, sm, s>>>(pp, b1, n, f, chunk, a, m);
+        else k_bias_gelu_cm_rows<4><<<gr, 256, sm, s>>>(pp, b1, n, f, chunk, a, m);
+        return cudaGetLastError();
+    }
     dim3 g((unsigned)(f / 64), (unsigned)((chunk + 63) / 64), (unsigned)(batch * (n / chunk)));
     k_bias_gelu_cm<<<g, 256, 0, s>>>((const __nv_bfloat16*)pre, b1, n, f, chunk,
                                      (__nv_bfloat16*)act, (__nv_bfloat16*)cm);
