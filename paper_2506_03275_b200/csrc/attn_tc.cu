@@ -41,7 +41,7 @@ using namespace csd::tc;
 
 // Debug timeline (scripts/attn_trace.py): when set, CTAs < kTraceCtas record SM clock64()
 // stamps at fixed slots (start, Q / K / V issue, S issue, softmax and epilogue phases).
-constexpr int kTraceCtas = 8, kTraceSlots = 256;
+constexpr int kTraceCtas = 8, kTraceSlots = 1024;
 __device__ uint64_t* g_attn_trace = nullptr;
 __device__ uint64_t* g_attn_span = nullptr;  // [grid][2] globaltimer at CTA start / end
 __device__ __forceinline__ uint64_t globaltimer_ns() {
@@ -62,7 +62,7 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 // Shared memory (runtime offsets in AttnParams, 1 KB-aligned regions):
 //   [Q: tile t strips of round_up(rows_t, 64) rows][X: staged base tile (sparse with base,
-//   chunk <= 192) or the colsum partials][K ring 2 x kKV][V ring 2 x kKV][ids 2 x 512 B][bars]
+//   chunk <= 192) or the colsum partials][K ring 2 x kKV][V ring 2 x kKV][row-half exchange][bars]
 // Q comes first: an M-tile with fewer than 128 live rows reads its 128 MMA rows past the end
 // of its strip (into the next strip / X) — dead rows whose P is never used.
 template <int E, int NT>
@@ -70,23 +70,18 @@ struct AttnLayout {
     static constexpr int kHalves = E / 64;
     static constexpr uint32_t kStrip = 128 * 128;  // 128 rows x 128 B
     static constexpr uint32_t kKV = kHalves * kStrip;  // one K or V block
-    static constexpr uint32_t kCsBytes = 2 * 4 * NT * 128 * 4;
-    static constexpr uint32_t kThreads = 128 + 128 * NT;
+    static constexpr uint32_t kCsBytes = 2 * 4 * NT * 128 * 4;  // colsum partials [2][NT][4][128]
+    static constexpr uint32_t kXchBytes = 2 * 128 * 2 * 4;       // row-half exchange [2][128][2]
+    // 4 control warps (producers, MMA, I/O) + 8 softmax warps: two per TMEM lane quadrant,
+    // each owning 64 of a row's 128 key columns
+    static constexpr uint32_t kThreads = 128 + 256;
     static constexpr uint32_t kTmemCols = (NT * 128 + NT * E) <= 256 ? 256 : 512;
     static constexpr uint32_t kMaxSmem = 227 * 1024;
 };
 
 struct AttnParams {
-    const __nv_bfloat16* k;  // copy mode: sparse K/V rows staged by cp.async
-    const __nv_bfloat16* v;
-    int64_t pitch;           // elements between consecutive token rows
-    int copy_mode;           // 1: sparse K/V rows by cp.async from the producer + idle warps
-    int ncopy;               // copy threads in copy mode
-    int live_t1;             // live softmax threads of the last M-tile (its bar_p arrivals)
     int stage_base;          // base tile staged in smem region X by TMA (epilogue in smem)
-    int sm_threads;          // threads in the softmax branch (barrier counts), TMA mode
-    int sm_threads_copy;     // ... in copy mode (idle softmax warps copy instead)
-    uint32_t off_x, off_k, off_v, off_ids, off_bar;  // smem region offsets
+    uint32_t off_x, off_k, off_v, off_xch, off_bar;  // smem region offsets
     uint32_t q_off[2], q_strip[2];  // per M-tile: Q region offset, bytes per 64-column strip
     int q_rows[2];           // per M-tile: Q rows loaded (multiple of 64)
     uint32_t x_strip;        // staged base: bytes per 64-column strip
@@ -142,48 +137,31 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     uint64_t* bar_p = bars + 11;   // [NT]
     uint64_t* bar_o = bars + 13;
     uint64_t* bar_qe = bars + 14;  // Q buffer free (all S MMAs of the item done)
-    uint64_t* bar_ids = bars + 15;  // [2] key-row table of ring slot s written (copy mode)
     uint64_t* bar_bf = bars + 17;   // staged base tile of the current live item landed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
     uint64_t* bar_xc = bars + 19;   // every live softmax warp combined its rows into X
-    int32_t* ids_tab = reinterpret_cast<int32_t*>(smem + p.off_ids);
     uint8_t* const sq = smem;
     uint8_t* const sx = smem + p.off_x;
     uint8_t* const sk = smem + p.off_k;
     uint8_t* const sv = smem + p.off_v;
-    // copy_mode 2: odd CTAs copy (LSU), even CTAs gather (TMA) -- TPC siblings split the paths
-    const bool cpm = !dense && (p.copy_mode == 1 || p.copy_mode == 3 || (p.copy_mode == 2 && (blockIdx.x & 1)));
-    const int sm_threads = cpm ? p.sm_threads_copy : p.sm_threads;
-    // copy_mode 3 (split): K by TMA gather4 from the producer warps, V by cp.async from the
-    // idle softmax warps -- the two staging paths run concurrently
-    const bool split = cpm && p.copy_mode == 3;
-
-    if (cpm) {
-        // partial key blocks copy only their live rows; the stale V rows they leave behind
-        // must be finite for P.V (P = 0 there): start from a zeroed V ring
-        for (int i = threadIdx.x; i < (int)(2 * L::kKV / 16); i += blockDim.x)
-            reinterpret_cast<uint4*>(sv)[i] = make_uint4(0u, 0u, 0u, 0u);
-        fence_proxy_async_smem();
-    }
     if (threadIdx.x == 0) {
+        // the host sizes the request without alignment slack (the 227 KB budget is tight)
+        if ((raw_u32 & 1023u) != 0) __trap();
         mbar_init(bar_q, 1);
         for (int i = 0; i < 2; ++i) {
-            // copy mode: one cp.async-tracking arrival per copy thread
-            mbar_init(bar_kf + i, (cpm && !split) ? p.ncopy : 1);
+            mbar_init(bar_kf + i, 1);
             mbar_init(bar_ke + i, 1);
-            mbar_init(bar_vf + i, cpm ? (split ? p.ncopy - 96 : p.ncopy) : 1);
+            mbar_init(bar_vf + i, 1);
             mbar_init(bar_ve + i, 1);
-            mbar_init(bar_ids + i, 1);
         }
         for (int t = 0; t < NT; ++t) {
             mbar_init(bar_s + t, 1);
-            // copy mode: the idle warps of tile 1 copy instead of zeroing their P rows
-            mbar_init(bar_p + t, (cpm && t == NT - 1) ? p.live_t1 : 128);
+            mbar_init(bar_p + t, 256);  // every softmax thread (dead rows write P = 0)
         }
         mbar_init(bar_o, 1);
         mbar_init(bar_qe, 1);
         mbar_init(bar_bf, 1);
-        mbar_init(bar_xc, sm_threads / 32);
+        mbar_init(bar_xc, 8);  // one arrival per softmax warp
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<L::kTmemCols>(tmem_slot);
@@ -244,19 +222,16 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         bulk_wait0();  // the last out tile has landed before the CTA exits
     };
     // ---------------------------------------------------------------- producers
-    // TMA mode: warps 0/2/3 spread the gather4s (one warp's TMA issue is serialised).
-    // Copy mode (sparse, idle softmax warps available): K/V rows by cp.async, 16-byte pieces,
-    // one row's pieces on consecutive copy threads (scripts/gather_bench2.cu: ~2.6x the
-    // per-SM rate of tile::gather4); warp 0 publishes each block's key-row table in smem.
-    auto producer = [&](int ct) {  // ct: copy-thread index (warp 0 lanes are 0..31)
+    // Warps 0/2/3 spread the sparse blocks' tile::gather4s (one warp's TMA issue is
+    // serialised); dense blocks are plain TMA tiles from warp 0.
+    auto producer = [&]() {
         const int pw = warp == 0 ? 0 : warp - 1;
-        const bool mine = warp <= 3 && (lane % 3) == pw;
+        const bool mine = (lane % 3) == pw;
         if (warp == 0 && lane == 0) {
             tma_prefetch_desc(&tm_q);
             tma_prefetch_desc(dense ? &tm_k : &tm_kg);
             tma_prefetch_desc(dense ? &tm_v : &tm_vg);
         }
-        constexpr int kPieces = E / 8;  // 16-byte pieces per key row
         uint32_t gb = 0, li = 0;
         for (int item = blockIdx.x; item < items; item += gridDim.x) {
             const int cnt = dense ? p.n : p.counts[item];
@@ -279,9 +254,8 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             const int32_t* ids = dense ? nullptr : p.idx + (int64_t)item * p.k_max;
             for (int j = 0; j < nblk; ++j, ++gb) {
                 const int s = gb & 1;
-                const int nvalid = min(128, cnt - j * 128);
                 int32_t rows[4] = {0, 0, 0, 0};
-                if (!dense && (warp == 0 || ((!cpm || split) && warp <= 3))) {
+                if (!dense) {
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
                         int r = j * 128 + lane * 4 + i;
@@ -290,51 +264,6 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                     }
                 }
                 if (gb >= 2) mbar_wait(bar_ke + s, ((gb >> 1) - 1) & 1);
-                if (cpm) {
-                    // slot s's table was read by block gb-2's copies: V of gb-2 consumed
-                    if (gb >= 2) mbar_wait(bar_ve + s, ((gb >> 1) - 1) & 1);
-                    if (warp == 0) {
-                        *reinterpret_cast<int4*>(ids_tab + s * 128 + lane * 4) =
-                            make_int4(rows[0], rows[1], rows[2], rows[3]);
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(bar_ids + s);
-                    }
-                    if (warp == 0 && lane == 0) ATTN_TRACE(16 + gb);
-                    if (split && warp <= 3) {
-                        // split mode: K rows by TMA gather4 (live 4-row groups, warps 0/2/3);
-                        // the idle softmax warps copy V with cp.async at the same time
-                        const int ngroups = (nvalid + 3) >> 2;
-                        if (warp == 0 && lane == 0)
-                            mbar_arrive_expect_tx(bar_kf + s, (uint32_t)ngroups * 4u * (uint32_t)E * 2u);
-                        if ((lane % 3) == pw && lane < ngroups)
-                            for (int hf = 0; hf < L::kHalves; ++hf)
-                                tma_gather4(&tm_kg, bar_kf + s, sk + s * L::kKV + hf * L::kStrip + lane * 512,
-                                            col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
-                        if (warp == 0 && lane == 0) ATTN_TRACE(48 + gb);
-                        continue;
-                    }
-                    mbar_wait(bar_ids + s, (gb >> 1) & 1);
-                    const int32_t* tab = ids_tab + s * 128;
-                    const int c0 = split ? ct - 96 : ct, cstride = split ? p.ncopy - 96 : p.ncopy;
-                    auto copy_rows = [&](const __nv_bfloat16* src_t, uint8_t* dst) {
-                        for (int idx = c0; idx < nvalid * kPieces; idx += cstride) {
-                            const int r = idx / kPieces, piece = idx - r * kPieces;
-                            const char* src = reinterpret_cast<const char*>(
-                                src_t + (int64_t)tab[r] * p.pitch + col0) + piece * 16;
-                            const uint32_t d = smem_u32(dst) + (piece >> 3) * L::kStrip + r * 128 +
-                                               (((piece & 7) ^ (r & 7)) << 4);
-                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-                        }
-                    };
-                    if (!split) {
-                        copy_rows(p.k, sk + s * L::kKV);
-                        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar_kf + s)) : "memory");
-                    }
-                    copy_rows(p.v, sv + s * L::kKV);
-                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar_vf + s)) : "memory");
-                    if (warp == 0 && lane == 0) ATTN_TRACE(48 + gb);
-                    continue;
-                }
                 // K_j -> ring slot s
                 if (warp == 0 && lane == 0) ATTN_TRACE(16 + gb);
                 if (warp == 0 && lane == 0) mbar_arrive_expect_tx(bar_kf + s, L::kKV);
@@ -368,11 +297,8 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             ++li;
         }
     };
-    // copy-thread numbering: warps 0, 2, 3 -> 0..95, then the idle softmax warps
-    const int sw_all = warp - 4;
-    const bool idle_sm = warp >= 4 && cpm && (((sw_all >> 2) * 128 + (warp & 3) * 32) >= p.chunk);
     if (warp == 0 || warp == 2 || warp == 3) {
-        producer(warp == 0 ? lane : (warp - 1) * 32 + lane);
+        producer();
     } else if (warp == 1) {
         if (lane == 1 && p.stage_base) io_thread();
         // ------------------------------------------------------------ MMA issuer
@@ -409,7 +335,6 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 mbar_wait(bar_q, li & 1);
                 ATTN_TRACE(8 + li);
                 mbar_wait(bar_kf + (gb & 1), (gb >> 1) & 1);
-                if (cpm) fence_proxy_async_smem();  // cp.async (generic proxy) -> tcgen05 reads
                 tc_fence_after();
                 ATTN_TRACE(80 + gb);
                 for (int t = 0; t < NT; ++t) issue_s(t, gb);
@@ -424,18 +349,20 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                         mbar_wait(bar_p + t, g & 1);
                         if (t == 0) {
                             mbar_wait(bar_vf + (g & 1), (g >> 1) & 1);
-                            if (cpm) fence_proxy_async_smem();
+                            ATTN_TRACE(832 + (g & 63));
                         }
                         tc_fence_after();
+                        ATTN_TRACE(640 + 64 * t + (g & 63));
                         issue_pv(t, g, j > 0);
                         if (t == NT - 1) mma_commit(bar_ve + (g & 1));
                         if (more) {
                             if (t == 0) {
                                 mbar_wait(bar_kf + ((g + 1) & 1), ((g + 1) >> 1) & 1);
-                                if (cpm) fence_proxy_async_smem();
                                 tc_fence_after();
                                 ATTN_TRACE(80 + g + 1);
+                                ATTN_TRACE(768 + ((g + 1) & 63));
                             }
+                            ATTN_TRACE(512 + 64 * t + ((g + 1) & 63));
                             issue_s(t, g + 1);  // in-order after PV_t(j): P_t consumed first
                             if (t == NT - 1) {
                                 mma_commit(bar_ke + ((g + 1) & 1));
@@ -449,24 +376,23 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 ++li;
             }
         }
-    } else if (idle_sm) {
-        // idle softmax warp (rows past the chunk) in copy mode: extra copy threads
-        const int first_idle = (p.chunk + 31) / 32;  // first idle softmax warp index
-        producer(96 + (sw_all - first_idle) * 32 + lane);
-    } else if (warp >= 4) {
+    } else {
         // ------------------------------------------------------------ softmax / epilogue
-        const int sw = warp - 4;          // 0 .. 4*NT-1
-        const int t = sw >> 2, quad = warp & 3;
-        const int row_t = quad * 32 + lane;
-        const int crow = t * 128 + row_t;  // row within the chunk
-        const bool row_ok = crow < p.chunk;
-        const bool warp_ok = (t * 128 + quad * 32) < p.chunk;
+        // 8 warps: warp 4 + 4 hf + quad owns TMEM lane quadrant `quad` (rows quad * 32 + lane
+        // of every M-tile) and key columns [64 hf, 64 hf + 64) of each S block.  The two
+        // halves of a row meet in smem (row max per block, row sum per item) behind a
+        // 64-thread named barrier per quadrant.  All 8 warps walk the M-tiles one after the
+        // other, so tile t's exponentials run at the full MUFU rate while the MMA pipe works
+        // on tile 1 - t (P.V then the next S).
+        const int sw = warp - 4;  // 0 .. 7
+        const int hf = sw >> 2, quad = sw & 3;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-        const uint32_t tS = tmem + lane_off + t * 128;
-        const uint32_t tO = tmem + lane_off + NT * 128 + t * E;
-        float* cs_part = reinterpret_cast<float*>(sx);
+        float* cs_part = reinterpret_cast<float*>(sx);  // [2][NT][4][128]
+        float* xch = reinterpret_cast<float*>(smem + p.off_xch);  // [2][128][2]
         const bool do_cs = p.colsum != nullptr;
         const float sl2 = p.qk_scale_log2;
+        const int qbar = 2 + quad;  // the quadrant's two warps
+        constexpr int kOc = E / 64;  // 32-column O groups per half
         uint32_t gb = 0, li = 0;
         for (int item = blockIdx.x; item < items; item += gridDim.x) {
             const int cnt = dense ? p.n : p.counts[item];
@@ -474,7 +400,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             const int b = bh / p.heads, h = bh % p.heads;
             if (cnt == 0) {  // pass base through (attention.cpp:169)
                 if (p.base != p.out && p.base != nullptr) {
-                    for (int r = threadIdx.x - 128; r < p.chunk * (E / 8); r += 128 * NT) {
+                    for (int r = threadIdx.x - 128; r < p.chunk * (E / 8); r += 256) {
                         const int row = r / (E / 8), v8 = r % (E / 8);
                         const int64_t off = tok_elem_off(p.layout, b, h, (int64_t)c * p.chunk + row,
                                                          p.heads, p.n, E) + v8 * 8;
@@ -485,162 +411,202 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 continue;
             }
             const int nblk = (cnt + 127) / 128;
-            const int64_t tok = (int64_t)c * p.chunk + crow;
-            float mpl = 0.f, inv_lp = 0.f;
-            if (do_cs && row_ok) {
-                const int64_t si = (int64_t)bh * p.n + tok;
-                mpl = p.prev_m[si] * kLog2e;
-                inv_lp = 1.0f / p.prev_l[si];
+            float m_run[NT], m_true[NT], l_run[NT], mpl[NT], inv_lp[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                m_run[t] = -INFINITY;
+                m_true[t] = -INFINITY;
+                l_run[t] = 0.f;
+                mpl[t] = 0.f;
+                inv_lp[t] = 0.f;
+                const int crow = t * 128 + quad * 32 + lane;
+                if (do_cs && crow < p.chunk) {
+                    const int64_t si = (int64_t)bh * p.n + (int64_t)c * p.chunk + crow;
+                    mpl[t] = p.prev_m[si] * kLog2e;
+                    inv_lp[t] = 1.0f / p.prev_l[si];
+                }
             }
-            float m_run = -INFINITY, m_true = -INFINITY, l_run = 0.f;
             for (int j = 0; j < nblk; ++j) {
                 const uint32_t g = gb + j;
-                mbar_wait(bar_s + t, g & 1);
-                tc_fence_after();
-                if (lane == 0 && sw == 0) ATTN_TRACE(144 + g);
                 const int ncols = min(128, cnt - j * 128);
-                if (warp_ok) {
-                    // S row in two 64-column halves (2 TMEM loads in flight, one wait each)
-                    // fast path (uniform): every column and every row of this warp is live
-                    const bool full = ncols == 128 && __all_sync(0xffffffffu, row_ok);
-                    const int ngrp = full ? 4 : (ncols + 31) >> 5;  // live 32-column groups
-                    // pass 1: row max over the live halves, four independent max chains
-                    float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+                const int nh = min(64, max(0, ncols - 64 * hf));  // live columns of this half
 #pragma unroll
-                    for (int hf = 0; hf < 2; ++hf) {
-                        if (hf * 2 >= ngrp) break;  // uniform
+                for (int t = 0; t < NT; ++t) {
+                    const int crow = t * 128 + quad * 32 + lane;
+                    const bool row_ok = crow < p.chunk;
+                    const bool warp_ok = t * 128 + quad * 32 < p.chunk;  // same for both halves
+                    const uint32_t tS = tmem + lane_off + t * 128;
+                    const uint32_t tO = tmem + lane_off + NT * 128 + t * E;
+                    mbar_wait(bar_s + t, g & 1);
+                    tc_fence_after();
+                    if (lane == 0 && sw == 0) ATTN_TRACE(144 + g);
+                    if (lane == 0 && quad == 0 && hf == 0) ATTN_TRACE(256 + 64 * t + (g & 63));
+                    if (warp_ok) {
+                        // this half's 64 S columns (2 TMEM loads in flight, one wait)
+                        const bool full = nh == 64 && __all_sync(0xffffffffu, row_ok);
                         uint32_t sr[64];
-                        tmem_ld32(tS + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-                        tmem_ld32(tS + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-                        tmem_ld_wait();
+                        if (nh > 0) {  // uniform
+                            tmem_ld32(tS + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+                            tmem_ld32(tS + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+                            tmem_ld_wait();
+                        }
                         if (!full) {
 #pragma unroll
                             for (int i = 0; i < 64; ++i)
-                                if (hf * 64 + i >= ncols) sr[i] = __float_as_uint(-INFINITY);
+                                if (i >= nh) sr[i] = __float_as_uint(-INFINITY);
                         }
+                        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
                         for (int i = 0; i < 64; i += 8)
 #pragma unroll
                             for (int u = 0; u < 4; ++u)
                                 mx4[u] = fmax3(mx4[u], __uint_as_float(sr[i + 2 * u]),
                                                __uint_as_float(sr[i + 2 * u + 1]));
-                    }
-                    const float mraw = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-                    const float mx = row_ok ? mraw * sl2 : -INFINITY;  // sl2 > 0: max commutes
-                    m_true = fmaxf(m_true, mx);
-                    const bool need = mx > m_run + kRescaleThreshold;
-                    const float alpha = need ? ex2_approx(m_run - mx) : 1.0f;
-                    if (need) {
-                        m_run = mx;
-                        l_run *= alpha;
-                    }
-                    if (j > 0 && __any_sync(0xffffffffu, need)) {  // PV_t(j-1) done (bar_s order)
-#pragma unroll 1
-                        for (int oc = 0; oc < E / 32; ++oc) {
-                            uint32_t r[32];
-                            tmem_ld32(tO + oc * 32, r);
-                            tmem_ld_wait();
-#pragma unroll
-                            for (int i = 0; i < 32; ++i)
-                                r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-                            tmem_st32(tO + oc * 32, r);
+                        const float mloc = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+                        // row max across the halves; slot t (NT = 2: the other tile's exchange
+                        // sits between two uses) or block parity (NT = 1)
+                        float* xr = xch + ((NT == 2 ? t : (int)(g & 1)) * 128 + quad * 32 + lane) * 2;
+                        xr[hf] = mloc;
+                        named_bar_sync(qbar, 64);
+                        const float mraw = fmaxf(mloc, xr[hf ^ 1]);
+                        const float mx = row_ok ? mraw * sl2 : -INFINITY;  // sl2 > 0: max commutes
+                        m_true[t] = fmaxf(m_true[t], mx);
+                        const bool need = mx > m_run[t] + kRescaleThreshold;
+                        const float alpha = need ? ex2_approx(m_run[t] - mx) : 1.0f;
+                        if (need) {
+                            m_run[t] = mx;
+                            l_run[t] *= alpha;
                         }
-                    }
-                    const float w = do_cs ? ex2_approx(m_run - mpl) * inv_lp : 0.f;
-                    const float neg_m = row_ok ? -m_run : -INFINITY;  // dead rows -> p = 0
-                    const float2 sl2v = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
-                    float2 part0 = make_float2(0.f, 0.f), part1 = make_float2(0.f, 0.f);
+                        if (j > 0 && __any_sync(0xffffffffu, need)) {  // PV_t(j-1) done (bar_s order)
+#pragma unroll 1
+                            for (int oc = 0; oc < kOc; ++oc) {
+                                uint32_t r[32];
+                                tmem_ld32(tO + (hf * kOc + oc) * 32, r);
+                                tmem_ld_wait();
 #pragma unroll
-                    for (int cc = 0; cc < 4; ++cc) {
-                        if (cc >= ngrp) {  // uniform: a fully masked group contributes P = 0
+                                for (int i = 0; i < 32; ++i)
+                                    r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+                                tmem_st32(tO + (hf * kOc + oc) * 32, r);
+                            }
+                        }
+                        const float w = do_cs ? ex2_approx(m_run[t] - mpl[t]) * inv_lp[t] : 0.f;
+                        const float neg_m = row_ok ? -m_run[t] : -INFINITY;  // dead rows -> p = 0
+                        const float2 sl2v = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
+                        float2 part0 = make_float2(0.f, 0.f), part1 = make_float2(0.f, 0.f);
+#pragma unroll
+                        for (int cc = 0; cc < 2; ++cc) {
+                            float* csp = cs_part + ((((g & 1) * NT + t) * 4 + quad) * 128) + hf * 64 + cc * 32;
+                            if (cc * 32 >= nh) {  // uniform: a fully masked group contributes P = 0
+                                uint32_t pk[16];
+#pragma unroll
+                                for (int q = 0; q < 16; ++q) pk[q] = 0u;
+                                tmem_st16(tS + hf * 32 + cc * 16, pk);
+                                if (do_cs) csp[lane] = 0.f;
+                                continue;
+                            }
+                            float pv[32];
+                            // 2^(S*scale - m) with paired FFMA2 / FADD2 (two row sums in flight)
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) {
+                                const float2 x = make_float2(__uint_as_float(sr[cc * 32 + 2 * q]),
+                                                             __uint_as_float(sr[cc * 32 + 2 * q + 1]));
+                                const float2 y = __ffma2_rn(x, sl2v, nm2);
+                                float2 e;
+                                e.x = ex2_approx(y.x);
+                                e.y = ex2_approx(y.y);
+                                pv[2 * q] = e.x;
+                                pv[2 * q + 1] = e.y;
+                                if (q & 1) part1 = __fadd2_rn(part1, e);
+                                else part0 = __fadd2_rn(part0, e);
+                            }
+                            // P_t (bf16 pairs) over S_t columns [32 hf + 16 cc, +16): both halves'
+                            // S loads completed before the exchange barrier
                             uint32_t pk[16];
 #pragma unroll
-                            for (int q = 0; q < 16; ++q) pk[q] = 0u;
-                            tmem_st16(tS + cc * 16, pk);
-                            if (do_cs) cs_part[((g & 1) * 4 * NT + sw) * 128 + cc * 32 + lane] = 0.f;
-                            continue;
-                        }
-                        uint32_t sr[32];
-                        tmem_ld32(tS + cc * 32, sr);
-                        tmem_ld_wait();
-                        float pv[32];
-                        // 2^(S*scale - m) with paired FFMA2 / FADD2 (two row sums in flight)
+                            for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(pv[2 * q], pv[2 * q + 1]);
+                            tmem_st16(tS + hf * 32 + cc * 16, pk);
+                            if (do_cs) {
+                                // transpose-reduce the warp's 32x32 block: lane ends with column `lane`
 #pragma unroll
-                        for (int q = 0; q < 16; ++q) {
-                            float2 x;
-                            x.x = (full || cc * 32 + 2 * q < ncols) ? __uint_as_float(sr[2 * q]) : -INFINITY;
-                            x.y = (full || cc * 32 + 2 * q + 1 < ncols) ? __uint_as_float(sr[2 * q + 1]) : -INFINITY;
-                            const float2 y = __ffma2_rn(x, sl2v, nm2);
-                            float2 e;
-                            e.x = ex2_approx(y.x);
-                            e.y = ex2_approx(y.y);
-                            pv[2 * q] = e.x;
-                            pv[2 * q + 1] = e.y;
-                            if (q & 1) part1 = __fadd2_rn(part1, e);
-                            else part0 = __fadd2_rn(part0, e);
+                                for (int i = 0; i < 32; ++i) pv[i] *= w;
+#pragma unroll
+                                for (int wd = 16; wd >= 1; wd >>= 1) {
+                                    const bool upper = (lane & wd) != 0;
+#pragma unroll
+                                    for (int i = 0; i < wd; ++i) {
+                                        const float send = upper ? pv[i] : pv[i + wd];
+                                        const float keep = upper ? pv[i + wd] : pv[i];
+                                        pv[i] = keep + __shfl_xor_sync(0xffffffffu, send, wd);
+                                    }
+                                }
+                                csp[lane] = pv[0];
+                            }
                         }
-                        // P_t (bf16 pairs) over S_t columns [16 cc, 16 cc + 16) — already read
+                        const float2 part = __fadd2_rn(part0, part1);
+                        l_run[t] += part.x + part.y;
+                    } else {
+                        // rows past the chunk: zero P so the padded MMA rows stay finite
                         uint32_t pk[16];
 #pragma unroll
-                        for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(pv[2 * q], pv[2 * q + 1]);
-                        tmem_st16(tS + cc * 16, pk);
-                        if (do_cs) {
-                            // transpose-reduce the warp's 32x32 block: lane ends with column `lane`
-#pragma unroll
-                            for (int i = 0; i < 32; ++i) pv[i] *= w;
-#pragma unroll
-                            for (int wd = 16; wd >= 1; wd >>= 1) {
-                                const bool upper = (lane & wd) != 0;
-#pragma unroll
-                                for (int i = 0; i < wd; ++i) {
-                                    const float send = upper ? pv[i] : pv[i + wd];
-                                    const float keep = upper ? pv[i + wd] : pv[i];
-                                    pv[i] = keep + __shfl_xor_sync(0xffffffffu, send, wd);
-                                }
-                            }
-                            cs_part[((g & 1) * 4 * NT + sw) * 128 + cc * 32 + lane] = pv[0];
-                        }
+                        for (int q = 0; q < 16; ++q) pk[q] = 0u;
+                        tmem_st16(tS + hf * 32, pk);
+                        tmem_st16(tS + hf * 32 + 16, pk);
                     }
-                    const float2 part = __fadd2_rn(part0, part1);
-                    l_run += part.x + part.y;
-                } else {
-                    // rows past the chunk: zero P so the padded MMA rows stay finite
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int q = 0; q < 16; ++q) pk[q] = 0u;
-#pragma unroll
-                    for (int cc = 0; cc < 4; ++cc) tmem_st16(tS + cc * 16, pk);
+                    tmem_st_wait();
+                    tc_fence_before();
+                    mbar_arrive(bar_p + t);
+                    if (lane == 0 && sw == 0) ATTN_TRACE(168 + g);
+                    if (lane == 0 && quad == 0 && hf == 0) ATTN_TRACE(384 + 64 * t + (g & 63));
                 }
-                tmem_st_wait();
-                tc_fence_before();
-                mbar_arrive(bar_p + t);
-                if (lane == 0 && sw == 0) ATTN_TRACE(168 + g);
                 if (do_cs) {
-                    named_bar_sync(1, 128 * NT);
+                    named_bar_sync(1, 256);
                     const int st = sw * 32 + lane;
                     if (st < 128 && st < ncols) {
                         float s = 0.f;
-                        for (int wsl = 0; wsl < 4 * NT; ++wsl)
-                            if (wsl * 32 < p.chunk) s += cs_part[((g & 1) * 4 * NT + wsl) * 128 + st];
+                        for (int t = 0; t < NT; ++t)
+                            for (int qd = 0; qd < 4; ++qd)
+                                if (t * 128 + qd * 32 < p.chunk)
+                                    s += cs_part[(((g & 1) * NT + t) * 4 + qd) * 128 + st];
                         p.colsum[((int64_t)bh * p.chunks + c) * p.n + j * 128 + st] = s;
                     }
                 }
             }
             // ------------------------------------------------------------ epilogue
+            // full row sums: the halves swap partial sums (the first barrier retires the last
+            // block's max exchange, the third this exchange before the next item reuses xch)
+            float l_full[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                l_full[t] = l_run[t];
+                if (t * 128 + quad * 32 < p.chunk) {
+                    float* xr = xch + (t * 128 + quad * 32 + lane) * 2;
+                    named_bar_sync(qbar, 64);
+                    xr[hf] = l_run[t];
+                    named_bar_sync(qbar, 64);
+                    l_full[t] = l_run[t] + xr[hf ^ 1];
+                    named_bar_sync(qbar, 64);
+                }
+            }
             const bool has_base = p.base != nullptr;
             if (p.stage_base) {
                 // out = base + scale * O / l (north_star item 5) with the item's base tile
                 // already in smem (TMA, issued at the end of the previous item's epilogue):
-                // each thread combines its row in place (bf16, swizzled), then each warp
-                // copies its 32 rows out row-contiguously (16-byte lanes).
+                // each thread combines its half row in place (bf16, swizzled); the I/O thread
+                // stores the tile by TMA.
                 mbar_wait(bar_o, li & 1);
                 mbar_wait(bar_bf, li & 1);
                 tc_fence_after();
                 if (lane == 0 && sw == 0) ATTN_TRACE(240 + li);
-                if (warp_ok) {
-                    const float fsc = p.scale / l_run;
 #pragma unroll
-                    for (int oc = 0; oc < E / 32; ++oc) {
+                for (int t = 0; t < NT; ++t) {
+                    const int crow = t * 128 + quad * 32 + lane;
+                    const bool row_ok = crow < p.chunk;
+                    if (t * 128 + quad * 32 >= p.chunk) continue;  // uniform per warp
+                    const uint32_t tO = tmem + lane_off + NT * 128 + t * E;
+                    const float fsc = p.scale / l_full[t];
+#pragma unroll
+                    for (int o2 = 0; o2 < kOc; ++o2) {
+                        const int oc = hf * kOc + o2;
                         uint32_t r[32];
                         tmem_ld32(tO + oc * 32, r);
                         tmem_ld_wait();
@@ -662,71 +628,73 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                             *ptr = make_uint4(o4[0], o4[1], o4[2], o4[3]);
                         }
                     }
-                    if (lane == 0 && sw == 0) ATTN_TRACE(232 + li);
-                    if (row_ok && p.row_max != nullptr) {
-                        const int64_t si = (int64_t)bh * p.n + tok;
-                        p.row_max[si] = m_true * kLn2;
-                        p.exp_sum[si] = l_run * exp2f(m_run - m_true);
+                    if (row_ok && hf == 0 && p.row_max != nullptr) {
+                        const int64_t si = (int64_t)bh * p.n + (int64_t)c * p.chunk + crow;
+                        p.row_max[si] = m_true[t] * kLn2;
+                        p.exp_sum[si] = l_full[t] * exp2f(m_run[t] - m_true[t]);
                     }
                 }
+                if (lane == 0 && sw == 0) ATTN_TRACE(232 + li);
                 // hand X to the I/O thread (warp 1 lane 1): it stores the out tile by TMA and
                 // refills X with the next live item's base tile; the softmax warps go on
                 fence_proxy_async_smem();  // this thread's in-place writes -> async proxy
                 __syncwarp();
                 if (lane == 0) mbar_arrive(bar_xc);
             } else {
-            const int64_t off = tok_elem_off(p.layout, b, h, tok, p.heads, p.n, E);
-            uint4 bpre[E / 8];  // prefetch base while the last P.V runs
-            if (warp_ok && row_ok && has_base) {
-                const uint4* bp = reinterpret_cast<const uint4*>(p.base + off);
+                mbar_wait(bar_o, li & 1);
+                tc_fence_after();
+                if (lane == 0 && sw == 0) ATTN_TRACE(240 + li);
 #pragma unroll
-                for (int q = 0; q < E / 8; ++q) bpre[q] = __ldg(bp + q);
-            }
-            mbar_wait(bar_o, li & 1);
-            tc_fence_after();
-            if (lane == 0 && sw == 0) ATTN_TRACE(240 + li);
-            if (warp_ok) {
-                const float inv_l = 1.0f / l_run;
+                for (int t = 0; t < NT; ++t) {
+                    const int crow = t * 128 + quad * 32 + lane;
+                    const bool row_ok = crow < p.chunk;
+                    if (t * 128 + quad * 32 >= p.chunk) continue;  // uniform per warp
+                    const uint32_t tO = tmem + lane_off + NT * 128 + t * E;
+                    const int64_t tok = (int64_t)c * p.chunk + crow;
+                    const int64_t off = tok_elem_off(p.layout, b, h, tok, p.heads, p.n, E);
+                    const float inv_l = 1.0f / l_full[t];
 #pragma unroll
-                for (int oc = 0; oc < E / 32; ++oc) {
-                    uint32_t r[32];
-                    tmem_ld32(tO + oc * 32, r);
-                    tmem_ld_wait();
-                    if (row_ok) {
-                        float o[32];
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(r[i]) * inv_l;
+                    for (int o2 = 0; o2 < kOc; ++o2) {
+                        const int oc = hf * kOc + o2;
+                        uint32_t r[32];
+                        tmem_ld32(tO + oc * 32, r);
+                        tmem_ld_wait();
+                        if (!row_ok) continue;
+                        uint4 bq[4];
                         if (has_base) {
+                            const uint4* bp = reinterpret_cast<const uint4*>(p.base + off + oc * 32);
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const __nv_bfloat162* b2 =
-                                    reinterpret_cast<const __nv_bfloat162*>(&bpre[oc * 4 + q]);
-#pragma unroll
-                                for (int u = 0; u < 4; ++u) {
-                                    const float2 f = __bfloat1622float2(b2[u]);
-                                    o[q * 8 + 2 * u] = f.x + p.scale * o[q * 8 + 2 * u];
-                                    o[q * 8 + 2 * u + 1] = f.y + p.scale * o[q * 8 + 2 * u + 1];
-                                }
-                            }
+                            for (int q = 0; q < 4; ++q) bq[q] = __ldg(bp + q);
                         }
                         uint4* dp = reinterpret_cast<uint4*>(p.out + off + oc * 32);
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
+                            float o[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) o[i] = __uint_as_float(r[q * 8 + i]) * inv_l;
+                            if (has_base) {
+                                const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bq[q]);
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const float2 f = __bfloat1622float2(b2[u]);
+                                    o[2 * u] = f.x + p.scale * o[2 * u];
+                                    o[2 * u + 1] = f.y + p.scale * o[2 * u + 1];
+                                }
+                            }
                             uint4 v;
-                            v.x = pack_bf16x2(o[q * 8 + 0], o[q * 8 + 1]);
-                            v.y = pack_bf16x2(o[q * 8 + 2], o[q * 8 + 3]);
-                            v.z = pack_bf16x2(o[q * 8 + 4], o[q * 8 + 5]);
-                            v.w = pack_bf16x2(o[q * 8 + 6], o[q * 8 + 7]);
+                            v.x = pack_bf16x2(o[0], o[1]);
+                            v.y = pack_bf16x2(o[2], o[3]);
+                            v.z = pack_bf16x2(o[4], o[5]);
+                            v.w = pack_bf16x2(o[6], o[7]);
                             dp[q] = v;
                         }
                     }
+                    if (row_ok && hf == 0 && p.row_max != nullptr) {
+                        const int64_t si = (int64_t)bh * p.n + tok;
+                        p.row_max[si] = m_true[t] * kLn2;
+                        p.exp_sum[si] = l_full[t] * exp2f(m_run[t] - m_true[t]);
+                    }
                 }
-                if (row_ok && p.row_max != nullptr) {
-                    const int64_t si = (int64_t)bh * p.n + tok;
-                    p.row_max[si] = m_true * kLn2;
-                    p.exp_sum[si] = l_run * exp2f(m_run - m_true);
-                }
-            }
             }
             if (lane == 0 && sw == 0) ATTN_TRACE(248 + li);
             tc_fence_before();  // O reads ordered before the next item's bar_p arrive
@@ -794,22 +762,6 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
         !make_map_bf16(&tvg, a.v, cols, rows, cols, 1))
         return cudaErrorInvalidValue;
     AttnParams p{};
-    p.k = static_cast<const __nv_bfloat16*>(a.k);
-    p.v = static_cast<const __nv_bfloat16*>(a.v);
-    p.pitch = (int64_t)cols;
-    {
-        // copy mode needs >= 2 idle softmax warps (rows past the chunk in the last M-tile)
-        const int idle = 4 * NT - (int)((a.chunk + 31) / 32);
-        static const int env = [] {
-            // default: TMA tile::gather4 (measured faster end to end at FLUX: 63.5 vs 66 us;
-            // cp.async copies contend with the softmax warps); CSD_ATTN_COPY=1 selects copies
-            const char* e = std::getenv("CSD_ATTN_COPY");
-            return e != nullptr ? std::atoi(e) : 0;
-        }();
-        p.copy_mode = (a.idx != nullptr && idle >= 2) ? env : 0;
-        p.ncopy = 96 + 32 * idle;
-        p.live_t1 = (int)std::min<int64_t>(128, ((a.chunk - 128 * (NT - 1)) + 31) / 32 * 32);
-    }
     p.idx = a.idx;
     p.counts = a.counts;
     p.k_max = a.k_max;
@@ -828,6 +780,7 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
     p.chunks = (int)(a.n / a.chunk);
     p.items = (int)(a.batch * a.heads * p.chunks);
     p.qk_scale_log2 = kLog2e / std::sqrt((float)E);
+
     // ---- shared-memory layout (see AttnLayout)
     {
         auto al = [](uint32_t v) { return (v + 1023u) & ~1023u; };
@@ -841,7 +794,9 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
         }
         const uint32_t xrows = (uint32_t)((a.chunk + 63) / 64 * 64);
         const uint32_t xbase = L::kHalves * xrows * 128u;
-        const uint32_t tail = 4 * L::kKV + 2 * 512 + 256 + 1024;  // rings, ids, bars, align slack
+        // rings, row-half exchange, barriers (the dynamic smem window is 1 KB aligned: no
+        // slack, the kernel traps otherwise)
+        const uint32_t tail = 4 * L::kKV + L::kXchBytes + 256;
         const bool want = a.base != nullptr && a.colsum == nullptr && off + xbase + tail <= L::kMaxSmem;
         p.stage_base = want ? 1 : 0;
         p.x_strip = xrows * 128u;
@@ -849,13 +804,10 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
         off = al(off + (want ? std::max(xbase, L::kCsBytes) : L::kCsBytes));
         p.off_k = off;
         p.off_v = off + 2 * L::kKV;
-        p.off_ids = p.off_v + 2 * L::kKV;
-        p.off_bar = p.off_ids + 2 * 512;
-        // softmax-branch threads without / with copy mode (idle warps become copy threads)
-        p.sm_threads = 128 * NT;
-        p.sm_threads_copy = (int)((std::min<int64_t>(128 * NT, a.chunk) + 31) / 32 * 32);
+        p.off_xch = p.off_v + 2 * L::kKV;
+        p.off_bar = p.off_xch + L::kXchBytes;
     }
-    const uint32_t smem_bytes = p.off_bar + 256 + 1024;
+    const uint32_t smem_bytes = p.off_bar + 256;
     if (smem_bytes > L::kMaxSmem) return cudaErrorNotSupported;
     auto kern = k_attn_tc<E, NT>;
     static bool attr_done = false;  // once per instantiation (keeps graph capture clean)

@@ -17,7 +17,7 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2506_03275_b200 import _capi, ops  # noqa: E402
 
-SLOTS = 256
+SLOTS = 1024
 GHZ = 1.965
 
 
