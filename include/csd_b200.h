@@ -181,6 +181,30 @@ csd_status csd_project(csd_ctx* ctx, csd_mode mode, const void* x, const void* w
 csd_status csd_add(csd_ctx* ctx, csd_mode mode, const void* a, const void* b, int64_t numel,
                    void* out, void* stream);
 
+/* ----------------------------------------------------------- generation --
+ * The multi-step schedule driver's pieces.
+ *
+ * csd_resolve_schedule replaces csd::resolve_schedule (schedule.cpp:44-87, with the
+ * StepSchedule::validate invariants :21-41): modes[total_steps] receives csd_step_mode
+ * values — a dense refresh at step 0 and every (dense_interval + 1) boundary, sparse in
+ * between; with the step cache, steps of the centred `window` that are off the `stride`
+ * grid are skipped (step 0 never is).  Host-only; CSD_ERR_CONFIG on the reference's
+ * ConfigError cases. */
+typedef enum { CSD_STEP_DENSE = 0, CSD_STEP_SPARSE = 1, CSD_STEP_SKIPPED = 2 } csd_step_mode;
+csd_status csd_resolve_schedule(int64_t total_steps, int64_t dense_interval, int use_step_cache,
+                                int64_t window, int64_t stride, int32_t* modes);
+/* latent[i] += a * y[i] (harness.cpp:24-30, the per-step update at :200).  The latent is
+ * an fp32 master in both modes; y is the model output (fp32 CHECK, bf16 PROD).  PROD also
+ * writes bf16(latent) into latent_bf16 when non-null (the next step's block input). */
+csd_status csd_latent_axpy(csd_ctx* ctx, csd_mode mode, float* latent, float a, const void* y,
+                           int64_t numel, void* latent_bf16, void* stream);
+/* R^2 of (truth - origin) vs (approx - origin), fp32 inputs, double accumulation
+ * (metrics.cpp:5-30 over the harness.cpp:32-38 deltas; origin may be NULL).  Deterministic
+ * device reduction; synchronises `stream` and writes *r2 on the host.  CSD_ERR_NUMERIC when
+ * the true delta has zero variance (the reference's NumericError). */
+csd_status csd_r_squared(csd_ctx* ctx, const float* truth, const float* approx,
+                         const float* origin, int64_t numel, double* r2, void* stream);
+
 /* ---------------------------------------------------------------- block --
  * One DiT block (model.cpp:178-216: x += attn(x Wq, x Wk, x Wv) Wo;
  * x += mlp(x)) with device-resident weights and per-layer caches

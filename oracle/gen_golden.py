@@ -157,6 +157,33 @@ def main():
         ms[f"y{t}"] = cur
     ms["dense"] = M.dense(x)
     np.savez_compressed(os.path.join(OUT, "model_stack.npz"), **ms)
+
+    # ---- generation driver (harness.cpp:123-224, schedule.cpp:44-87):
+    # 2-layer desk model, 12 steps, dense every 4th, step cache window 6 stride 2
+    cfg = dict(batch=1, grid=(2, 8, 8), dim=64, head_dim=16, heads=4, hidden=128, layers=2,
+               voxel=(1, 2, 2), chunk=4, seed=1234)
+    sched = dict(total_steps=12, dense_interval=3, step_cache=True, window=6, stride=2,
+                 attn_k=8, mlp_k=32)
+    modes, r2, e2e, fin = O.run_generation(cfg, sched)
+    M = O.RefModel(cfg)
+    gen = {"cfg_grid": np.array(cfg["grid"]), "cfg_voxel": np.array(cfg["voxel"]),
+           "cfg_misc": np.array([cfg["batch"], cfg["dim"], cfg["head_dim"], cfg["heads"],
+                                 cfg["hidden"], cfg["layers"], cfg["chunk"], cfg["seed"]]),
+           "sched": np.array([sched[k] for k in ("total_steps", "dense_interval", "step_cache",
+                                                 "window", "stride", "attn_k", "mlp_k")]),
+           "grid0": g(cfg["seed"] + 1, (cfg["batch"], *cfg["grid"], cfg["dim"])),  # harness.cpp:16-22
+           "modes": modes, "latent_r2": r2, "e2e_r2": np.array([e2e]), "final": fin}
+    for layer in range(cfg["layers"]):
+        for kname, val in M.weights(layer).items():
+            gen[f"l{layer}_{kname}"] = val
+    np.savez_compressed(os.path.join(OUT, "generation.npz"), **gen)
+    # schedule cases (schedule.cpp): (total, interval, cache, window, stride) -> modes
+    cases = [(1, 0, 0, 0, 1), (20, 10, 0, 0, 1), (50, 10, 1, 30, 4), (12, 3, 1, 6, 2),
+             (7, 0, 1, 7, 3), (9, 2, 1, 1, 1), (30, 4, 1, 10, 1)]
+    sc = {"cases": np.array(cases, np.int64)}
+    for i, cs in enumerate(cases):
+        sc[f"modes{i}"] = O.resolve_schedule(*cs)
+    np.savez_compressed(os.path.join(OUT, "schedule.npz"), **sc)
     for fn in sorted(os.listdir(OUT)):
         print(fn, os.path.getsize(os.path.join(OUT, fn)))
 

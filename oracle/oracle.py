@@ -280,6 +280,37 @@ class RefModel:
         return idx, cnt
 
 
+def resolve_schedule(total_steps, dense_interval, step_cache=False, window=0, stride=1):
+    """schedule.cpp:44-87 through the reference library: modes (0 dense, 1 sparse, 2 skipped)."""
+    lib = C.CDLL(REF_LIB)
+    modes = np.zeros(max(int(total_steps), 1), np.int32)
+    _chk(lib.ref_resolve_schedule(_L(total_steps), _L(dense_interval), C.c_int(int(step_cache)),
+                                  _L(window), _L(stride), _i32(modes)))
+    return modes
+
+
+def run_generation(cfg: dict, sched: dict):
+    """harness.cpp:123-224 (run_generation, sparse-delta mode) through the reference library.
+
+    Returns (modes, per-step latent R^2, end-to-end R^2, decoded final latent [B,T,H,W,D])."""
+    lib = C.CDLL(REF_LIB)
+    c = cfg
+    cv = np.array([c["batch"], *c["grid"], c["dim"], c["head_dim"], c["heads"], c["hidden"],
+                   c["layers"], *c["voxel"], c["chunk"], c["seed"]], np.int64)
+    sv = np.array([sched["total_steps"], sched["dense_interval"], int(sched["step_cache"]),
+                   sched["window"], sched["stride"], sched["attn_k"], sched["mlp_k"]], np.int64)
+    t = int(sched["total_steps"])
+    modes = np.zeros(t, np.int32)
+    r2 = np.zeros(t, np.float64)
+    e2e = np.zeros(1, np.float64)
+    out = np.zeros((c["batch"], *c["grid"], c["dim"]), np.float32)
+    p64 = C.POINTER(C.c_int64)
+    pd = C.POINTER(C.c_double)
+    _chk(lib.ref_run_generation(cv.ctypes.data_as(p64), sv.ctypes.data_as(p64), _i32(modes),
+                                r2.ctypes.data_as(pd), e2e.ctypes.data_as(pd), _f(out)))
+    return modes, r2, float(e2e[0]), out
+
+
 def gaussian(seed: int, shape, std: float = 1.0) -> np.ndarray:
     """tests/test_util.hpp:50-55 random_tensor, bit-identical (needs the reference lib)."""
     lib = C.CDLL(REF_LIB)

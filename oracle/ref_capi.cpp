@@ -11,14 +11,21 @@
 // raw row-major buffers into csd_ref::Tensor, calls the reference function
 // named in its comment, and copies the result out.  Exceptions are mapped to
 // the same negative codes as oracle/csd_oracle.h.
+#include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
+#include <string>
+#include <unistd.h>
 #include <vector>
 
 #include "csd/attention.hpp"
 #include "csd/error.hpp"
+#include "csd/harness.hpp"
 #include "csd/mlp.hpp"
+#include "csd/schedule.hpp"
+#include "csd/tensor_io.hpp"
 #include "csd/model.hpp"
 #include "csd/rng.hpp"
 #include "csd/sparse_index.hpp"
@@ -295,6 +302,58 @@ int ref_model_indices(void* h, int64_t layer, int mlp, int32_t* idx, int32_t* co
     std::memcpy(idx, s.indices.data(), sizeof(int32_t) * s.indices.size());
     std::memcpy(counts, s.counts.data(), sizeof(int32_t) * s.counts.size());
     return static_cast<int>(s.k_max);
+}
+
+
+// schedule.cpp:44-87 -> modes[total_steps] (0 dense, 1 sparse, 2 skipped)
+int ref_resolve_schedule(int64_t total_steps, int64_t dense_interval, int step_cache,
+                         int64_t window, int64_t stride, int32_t* modes) {
+    return guard([&] {
+        const StepSchedule s = resolve_schedule(total_steps, dense_interval, step_cache != 0,
+                                                window, stride);
+        for (int64_t i = 0; i < total_steps; ++i)
+            modes[i] = static_cast<int32_t>(s.modes[static_cast<size_t>(i)]);
+    });
+}
+
+// harness.cpp:123-224 (run_generation, RunMode::SparseDelta): the seeded toy model and
+// latent of `cfg`, the resolved schedule, x += (1/T) * model output per step (skipped steps
+// reuse the last output), latent R^2 vs the dense trajectory per step.  Outputs: modes,
+// per-step latent R^2 (NaN when undefined), end-to-end R^2, and the decoded final latent
+// [B, T, H, W, D] (read back from the reference's own CSDT dump, tensor_io.cpp).
+// cfg = {batch, grid_t, grid_h, grid_w, dim, head_dim, heads, hidden, layers, voxel_t,
+//        voxel_h, voxel_w, chunk, seed}; sch = {total_steps, dense_interval, step_cache,
+//        window, stride, attn_k, mlp_k}
+int ref_run_generation(const int64_t* cfg, const int64_t* sch, int32_t* modes, double* latent_r2,
+                       double* e2e_r2, float* final_latent) {
+    return guard([&] {
+        RunRequest req;
+        ModelConfig& m = req.model;
+        m.batch = cfg[0]; m.grid_t = cfg[1]; m.grid_h = cfg[2]; m.grid_w = cfg[3];
+        m.model_dim = cfg[4]; m.head_dim = cfg[5]; m.heads = cfg[6]; m.mlp_hidden = cfg[7];
+        m.layers = cfg[8]; m.voxel_t = cfg[9]; m.voxel_h = cfg[10]; m.voxel_w = cfg[11];
+        m.chunk = cfg[12]; m.seed = static_cast<uint64_t>(cfg[13]);
+        req.schedule.total_steps = sch[0];
+        req.schedule.dense_interval = sch[1];
+        req.schedule.step_cache = sch[2] != 0;
+        req.schedule.window = sch[3];
+        req.schedule.stride = sch[4];
+        req.sparsity.attn_k = sch[5];
+        req.sparsity.mlp_k = sch[6];
+        req.mode = RunMode::SparseDelta;
+        char path[] = "/tmp/csd_ref_latent_XXXXXX";
+        const int fd = mkstemp(path);
+        if (fd >= 0) close(fd);
+        req.save_latent_path = path;
+        const RunReport rep = run_generation(req);
+        for (size_t i = 0; i < rep.steps.size(); ++i) {
+            modes[i] = static_cast<int32_t>(rep.steps[i].mode);
+            latent_r2[i] = rep.steps[i].latent_r2.value_or(std::nan(""));
+        }
+        *e2e_r2 = rep.end_to_end_r2.value_or(std::nan(""));
+        put(load_tensor(std::string(path)), final_latent);
+        std::remove(path);
+    });
 }
 
 }  // extern "C"

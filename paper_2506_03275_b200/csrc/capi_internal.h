@@ -25,6 +25,7 @@ enum WsSlot {
     kWsAct,
     kWsIdx,
     kWsCounts,
+    kWsR2,
     kWsCount
 };
 
