@@ -298,32 +298,54 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         }
     };
     if (warp == 0 || warp == 2 || warp == 3) {
-        producer();
+        // warp 3 lane 31 issues no gathers (lane % 3 != 2): it runs the staged-base I/O
+        if (warp == 3 && lane == 31) {
+            if (p.stage_base) io_thread();
+        } else {
+            producer();
+        }
     } else if (warp == 1) {
-        if (lane == 1 && p.stage_base) io_thread();
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        // The whole warp walks the schedule so the descriptors are warp-uniform (uniform
+        // registers, no per-MMA broadcast); lane 0 (elect.sync's leader) issues every MMA
+        // and commit, so the commits track that lane's MMAs.
+        {
             constexpr uint32_t idS = idesc_bf16(128, 128, false, false);
             constexpr uint32_t idO = idesc_bf16(128, E, false, true);
             const uint32_t sQ = smem_u32(sq), sK = smem_u32(sk);
             const uint32_t sV = smem_u32(sv);
+            auto commit = [&](uint64_t* b) {
+                if (elect_one()) mma_commit(b);
+                __syncwarp();
+            };
             auto issue_s = [&](int t, uint32_t g) {  // S_t = Q_t K_g^T
                 const uint32_t kb = sK + (g & 1) * L::kKV;
+                uint64_t da[E / 16], db[E / 16];
 #pragma unroll
-                for (int kk = 0; kk < E / 16; ++kk)
-                    mma_bf16(tmem + t * 128,
-                             desc_kmajor_sw128(sQ + p.q_off[t] + (kk / 4) * p.q_strip[t] + (kk % 4) * 32),
-                             desc_kmajor_sw128(kb + (kk / 4) * L::kStrip + (kk % 4) * 32), idS,
-                             kk > 0 ? 1u : 0u);
-                mma_commit(bar_s + t);
+                for (int kk = 0; kk < E / 16; ++kk) {
+                    da[kk] = desc_kmajor_sw128(sQ + p.q_off[t] + (kk / 4) * p.q_strip[t] + (kk % 4) * 32);
+                    db[kk] = desc_kmajor_sw128(kb + (kk / 4) * L::kStrip + (kk % 4) * 32);
+                }
+                if (elect_one()) {
+#pragma unroll
+                    for (int kk = 0; kk < E / 16; ++kk)
+                        mma_bf16(tmem + t * 128, da[kk], db[kk], idS, kk > 0 ? 1u : 0u);
+                    mma_commit(bar_s + t);
+                }
+                __syncwarp();
             };
             auto issue_pv = [&](int t, uint32_t g, bool acc) {  // O_t (+)= P_t V_g
                 const uint32_t vb = sV + (g & 1) * L::kKV;
+                uint64_t dv[8];
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    mma_bf16_ts(tmem + NT * 128 + t * E, tmem + t * 128 + kk * 8,
-                                desc_mnmajor_sw128(vb + kk * 2048, L::kStrip), idO,
-                                (acc || kk > 0) ? 1u : 0u);
+                for (int kk = 0; kk < 8; ++kk) dv[kk] = desc_mnmajor_sw128(vb + kk * 2048, L::kStrip);
+                if (elect_one()) {
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        mma_bf16_ts(tmem + NT * 128 + t * E, tmem + t * 128 + kk * 8, dv[kk], idO,
+                                    (acc || kk > 0) ? 1u : 0u);
+                }
+                __syncwarp();
             };
             uint32_t gb = 0, li = 0;
             for (int item = blockIdx.x; item < items; item += gridDim.x) {
@@ -338,8 +360,8 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 tc_fence_after();
                 ATTN_TRACE(80 + gb);
                 for (int t = 0; t < NT; ++t) issue_s(t, gb);
-                mma_commit(bar_ke + (gb & 1));
-                if (nblk == 1) mma_commit(bar_qe);
+                commit(bar_ke + (gb & 1));
+                if (nblk == 1) commit(bar_qe);
                 for (int j = 0; j < nblk; ++j) {
                     const uint32_t g = gb + j;
                     const bool more = j + 1 < nblk;
@@ -354,7 +376,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                         tc_fence_after();
                         ATTN_TRACE(640 + 64 * t + (g & 63));
                         issue_pv(t, g, j > 0);
-                        if (t == NT - 1) mma_commit(bar_ve + (g & 1));
+                        if (t == NT - 1) commit(bar_ve + (g & 1));
                         if (more) {
                             if (t == 0) {
                                 mbar_wait(bar_kf + ((g + 1) & 1), ((g + 1) >> 1) & 1);
@@ -365,13 +387,13 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                             ATTN_TRACE(512 + 64 * t + ((g + 1) & 63));
                             issue_s(t, g + 1);  // in-order after PV_t(j): P_t consumed first
                             if (t == NT - 1) {
-                                mma_commit(bar_ke + ((g + 1) & 1));
-                                if (j + 2 == nblk) mma_commit(bar_qe);
+                                commit(bar_ke + ((g + 1) & 1));
+                                if (j + 2 == nblk) commit(bar_qe);
                             }
                         }
                     }
                 }
-                mma_commit(bar_o);
+                commit(bar_o);
                 gb += nblk;
                 ++li;
             }

@@ -179,6 +179,20 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
         : "memory");
 }
+// One lane of a converged warp (elect.sync: the lowest active lane, i.e. lane 0 when the
+// whole warp runs) -- the warp computes the MMA operands uniformly (uniform registers) and
+// the elected lane issues.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t e = 0;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(e));
+    return e != 0;
+}
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile(
