@@ -204,6 +204,14 @@ csd_status csd_latent_axpy(csd_ctx* ctx, csd_mode mode, float* latent, float a, 
  * the true delta has zero variance (the reference's NumericError). */
 csd_status csd_r_squared(csd_ctx* ctx, const float* truth, const float* approx,
                          const float* origin, int64_t numel, double* r2, void* stream);
+/* index_set_to_masks (bitmask.cpp:55-85): one bitpacked mask per
+ * (b, h, chunk) row of an index set -- masks[rows][ceil(n_bits / 8)] bytes, bit i of byte j
+ * = element 8 j + i (bitmask.hpp:13-17), trailing pad bits zero.  Validates like the
+ * reference (ids in [0, n_bits) and unique -> CSD_ERR_INDEX; counts in [0, k_max] ->
+ * CSD_ERR_VALUE); synchronises `stream`. */
+csd_status csd_index_set_to_masks(csd_ctx* ctx, const int32_t* idx, const int32_t* counts,
+                                  int64_t rows, int64_t k_max, int64_t n_bits, uint8_t* masks,
+                                  void* stream);
 
 /* ---------------------------------------------------------------- block --
  * One DiT block (model.cpp:178-216: x += attn(x Wq, x Wk, x Wv) Wo;

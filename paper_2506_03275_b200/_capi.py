@@ -77,6 +77,7 @@ SIGNATURES = {
     "csd_resolve_schedule": (i32, [i64, i64, C.c_int, i64, i64, C.POINTER(C.c_int32)]),
     "csd_latent_axpy": (i32, [p, i32, fp, f32, fp, i64, fp, p]),
     "csd_r_squared": (i32, [p, fp, fp, fp, i64, C.POINTER(C.c_double), p]),
+    "csd_index_set_to_masks": (i32, [p, fp, fp, i64, i64, i64, fp, p]),
 }
 
 

@@ -1,9 +1,10 @@
-// generation.cu — the multi-step schedule driver's device pieces (SURVEY §8f rows 2 and 4).
+// generation.cu — the multi-step schedule driver's device pieces (SURVEY §8f rows 2-4).
 //
-//   csd_resolve_schedule : dense / sparse / skipped plan (schedule.cpp:44-87, validate :21-41)
-//   csd_latent_axpy      : latent += a * model_output (harness.cpp:24-30, used at :200)
-//   csd_r_squared        : R^2 of (truth - origin) vs (approx - origin) in double
-//                          (metrics.cpp:5-30 over harness.cpp:32-38 deltas)
+//   csd_resolve_schedule    : dense / sparse / skipped plan (schedule.cpp:44-87, :21-41)
+//   csd_latent_axpy         : latent += a * model_output (harness.cpp:24-30, used at :200)
+//   csd_r_squared           : R^2 of (truth - origin) vs (approx - origin) in double
+//                             (metrics.cpp:5-30 over harness.cpp:32-38 deltas)
+//   csd_index_set_to_masks  : bitpacked per-chunk masks of an index set (bitmask.cpp:55-85)
 //
 // The latent is an fp32 master in both modes (the reference keeps fp32); in PROD the block
 // output is bf16 and the axpy also refreshes a bf16 shadow copy that feeds the next step's
@@ -115,10 +116,59 @@ __global__ void k_r2_final(int pass, int nblocks, double* ws) {
     else ws[1] = s1 == 0.0 ? __longlong_as_double(0x7ff8000000000000ll) : 1.0 - s0 / s1;
 }
 
+// One CTA per (b, h, chunk) row: the row's n-bit mask is built in shared memory (32-bit
+// words, atomicOr), checked (popcount == count, else a duplicate; ids in [0, n)), and
+// written out as ceil(n / 8) bytes, LSB-first (bitmask.hpp:13-17) -- byte j of a
+// little-endian word w is bits [8 j, 8 j + 8) of it.
+__global__ void k_index_masks(const int32_t* __restrict__ idx, const int32_t* __restrict__ counts,
+                              int64_t k_max, int64_t n, int64_t row_bytes,
+                              uint8_t* __restrict__ masks, uint32_t* __restrict__ flags) {
+    extern __shared__ uint32_t bits[];
+    const int64_t row = blockIdx.x;
+    const int64_t nw = (n + 31) / 32;
+    for (int64_t w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0u;
+    __syncthreads();
+    const int cnt = counts[row];
+    if (cnt < 0 || cnt > k_max) {
+        if (threadIdx.x == 0) atomicOr(flags, kFlagCountRange);
+        return;
+    }
+    const int32_t* ids = idx + row * k_max;
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+        const int32_t id = ids[j];
+        if (id < 0 || id >= n) {
+            atomicOr(flags, kFlagIndexRange);
+            continue;
+        }
+        atomicOr(&bits[id >> 5], 1u << (id & 31));
+    }
+    __syncthreads();
+    int pc = 0;
+    for (int64_t w = threadIdx.x; w < nw; w += blockDim.x) pc += __popc(bits[w]);
+    for (int o = 16; o > 0; o >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, o);
+    __shared__ int warp_pc[32];
+    if ((threadIdx.x & 31) == 0) warp_pc[threadIdx.x >> 5] = pc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += warp_pc[w];
+        if (tot != cnt) atomicOr(flags, kFlagIndexDup);  // (out-of-range ids already flagged)
+    }
+    const uint8_t* b8 = reinterpret_cast<const uint8_t*>(bits);
+    uint8_t* dst = masks + row * row_bytes;
+    for (int64_t j = threadIdx.x; j < row_bytes; j += blockDim.x) dst[j] = b8[j];
+}
+
 }  // namespace dev
 }  // namespace csd
 
 using csd::set_error;
+
+#define CSD_CU_(expr)                                                         \
+    do {                                                                      \
+        const cudaError_t e_ = (expr);                                        \
+        if (e_ != cudaSuccess) return csd::cuda_status(e_, "generation.cu"); \
+    } while (0)
 
 extern "C" {
 
@@ -202,6 +252,36 @@ csd_status csd_r_squared(csd_ctx* ctx, const float* truth, const float* approx,
     c->launches += 4;
     if (std::isnan(*r2)) return set_error(CSD_ERR_NUMERIC, "r_squared undefined: true delta has zero variance");
     return CSD_OK;
+}
+
+csd_status csd_index_set_to_masks(csd_ctx* ctx, const int32_t* idx, const int32_t* counts,
+                                  int64_t rows, int64_t k_max, int64_t n_bits, uint8_t* masks,
+                                  void* stream) {
+    if (!ctx) return set_error(CSD_ERR_VALUE, "null context");
+    if (rows < 0 || k_max < 0 || n_bits < 0)
+        return set_error(CSD_ERR_SHAPE, "index_set_to_masks: negative extent");
+    if (k_max > n_bits)
+        return set_error(CSD_ERR_VALUE, "mask length %lld smaller than index k_max %lld",
+                         (long long)n_bits, (long long)k_max);
+    if (rows == 0) return CSD_OK;
+    auto* c = reinterpret_cast<csd::Ctx*>(ctx);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t row_bytes = (n_bits + 7) / 8;
+    const size_t smem = (size_t)((n_bits + 31) / 32) * 4 + 4;
+    if (smem > 200 * 1024)
+        return set_error(CSD_ERR_UNSUPPORTED, "mask length %lld too long", (long long)n_bits);
+    static size_t attr = 48 * 1024;  // opt in once per larger size (keeps graph capture clean)
+    if (smem > attr) {
+        CSD_CU_(cudaFuncSetAttribute(csd::dev::k_index_masks,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = smem;
+    }
+    csd::dev::k_index_masks<<<(unsigned)rows, 256, smem, s>>>(idx, counts, k_max, n_bits,
+                                                              row_bytes, masks, c->flags);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return csd::cuda_status(e, "index_set_to_masks");
+    c->launches += 1;
+    return csd::check_flags(c, s);  // the reference validates first (IndexError / ValueError)
 }
 
 }  // extern "C"

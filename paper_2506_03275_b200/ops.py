@@ -174,6 +174,19 @@ class SparseIndexSet:
         context().sync()
 
 
+def index_set_to_masks(idx: SparseIndexSet, n: int) -> torch.Tensor:
+    """bitmask.cpp:55-85 on the device: uint8 [B, H, C, ceil(n / 8)], one LSB-first bitpacked
+    mask per (b, h, chunk) (bitmask.hpp:13-17); popcount of each row equals its count."""
+    from . import errors
+    if n < idx.domain:
+        raise errors.ValueError(f"mask length {n} smaller than index domain {idx.domain}")
+    out = torch.empty((idx.batch, idx.heads, idx.chunks, (n + 7) // 8), dtype=torch.uint8,
+                      device=idx.indices.device)
+    _call("csd_index_set_to_masks", _ptr(idx.indices), _ptr(idx.counts),
+          idx.batch * idx.heads * idx.chunks, idx.k_max, n, _ptr(out), _stream())
+    return out
+
+
 def select_top_k(scores: torch.Tensor, k: int, chunk_size: int) -> SparseIndexSet:
     """sparse_index.cpp:64-96 on a [B,H,C,M] float32 tensor."""
     from .errors import ShapeError
