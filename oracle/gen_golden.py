@@ -144,6 +144,23 @@ def main():
             bl[f"midx{t}"] = mi
     np.savez_compressed(os.path.join(OUT, "block.npz"), **bl)
 
+    # ---- static attention pattern (model.hpp:97-99, attention.hpp:50-52): applied verbatim
+    # on dense steps, ragged counts including 0 (test_attention.cpp:441-459); D S S D S
+    cfg = dict(batch=1, grid=(2, 8, 8), dim=64, head_dim=16, heads=4, hidden=128, layers=1,
+               voxel=(1, 2, 2), chunk=4, seed=1234)
+    M = O.RefModel(cfg)
+    rng = np.random.default_rng(441)
+    nc = M.n // cfg["chunk"]
+    sidx, scnt = random_index_set(rng, 1, cfg["heads"], nc, 8, M.n)
+    st = {"idx": sidx, "counts": scnt, "sched": np.array(sched)}
+    for kname, val in M.weights(0).items():
+        st["w_" + kname] = val
+    for t, dense in enumerate(sched):
+        xin = (xs + 0.05 * t * g(2000 + t, xs.shape)).astype(np.float32)
+        st[f"x{t}"] = xin
+        st[f"y{t}"] = M.step_static(xin, dense, attn_k, mlp_k, sidx, scnt)
+    np.savez_compressed(os.path.join(OUT, "block_static.npz"), **st)
+
     # ---- block stack through model_forward_step (model.hpp defaults, 2 layers), fed back
     # step to step like harness.cpp:186-212; tests/cpp/model_mirror.cpp replays it
     cfg = dict(batch=1, grid=(2, 8, 8), dim=64, head_dim=16, heads=4, hidden=128, layers=2,

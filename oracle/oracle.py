@@ -264,6 +264,17 @@ class RefModel:
                                      _L(mlp_k), _f(out)))
         return out
 
+    def step_static(self, x, dense, attn_k, mlp_k, idx, counts):
+        """model_forward_step with a static attention pattern (model.hpp:97-99)."""
+        x = f32(x)
+        out = np.empty_like(x)
+        idx = np.ascontiguousarray(idx, np.int32)
+        counts = np.ascontiguousarray(counts, np.int32)
+        _chk(self.lib.ref_model_step_static(C.c_void_p(self.h), _f(x), C.c_int(int(dense)),
+                                            _L(attn_k), _L(mlp_k), _i32(idx), _i32(counts),
+                                            _L(idx.shape[-1]), _f(out)))
+        return out
+
     def dense(self, x):
         x = f32(x)
         out = np.empty_like(x)

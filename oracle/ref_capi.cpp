@@ -273,6 +273,25 @@ int ref_model_step(void* h, const float* x, int dense, int64_t attn_k, int64_t m
     });
 }
 
+// model.cpp:178-216 with a static attention pattern (model.hpp:97-99, attention.hpp:50-52):
+// idx [B, H, C, k_max] / counts [B, H, C] replace the top-k on dense steps, verbatim.
+int ref_model_step_static(void* h, const float* x, int dense, int64_t attn_k, int64_t mlp_k,
+                          const int32_t* idx, const int32_t* counts, int64_t k_max, float* out) {
+    auto* m = static_cast<RefModel*>(h);
+    return guard([&] {
+        const auto& c = m->model.cfg;
+        SparsityConfig sp;
+        sp.attn_k = attn_k;
+        sp.mlp_k = mlp_k;
+        const int64_t chunks = c.seq_len() / c.chunk;
+        const SparseIndexSet st =
+            make_set(idx, counts, c.batch, c.heads, chunks, c.chunk, k_max, c.seq_len());
+        put(model_forward_step(m->model, m->state, make(x, {c.batch, c.seq_len(), c.model_dim}),
+                               dense != 0, sp, nullptr, &st),
+            out);
+    });
+}
+
 // model.cpp:167-176
 int ref_model_dense(void* h, const float* x, float* out) {
     auto* m = static_cast<RefModel*>(h);

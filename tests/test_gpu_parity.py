@@ -414,3 +414,60 @@ def test_prod_block_batch2_vs_check_mode(ops, port):
         for bb in range(b):
             err = rel_l2(N(yp)[bb] - x[bb], N(yc)[bb] - x[bb])
             assert err < REL_L2_TOL, (t, bb, err)
+
+
+def test_check_block_static_pattern_bit_exact(ops, golden):
+    """Static attention pattern (model.hpp:97-99, attention.hpp:50-52): applied verbatim on
+    dense steps, ragged counts including 0 (test_attention.cpp:441-459); the reference's
+    model_forward_step outputs reproduced bit-for-bit over D S S D S."""
+    g = golden("block_static")
+    gb = golden("block")
+    misc, grid = gb["cfg_misc"], gb["cfg_grid"]
+    n = int(np.prod(grid))
+    cfg = ops.BlockConfig(batch=int(misc[0]), seq=n, dim=int(misc[1]), heads=int(misc[3]),
+                          head_dim=int(misc[2]), hidden=int(misc[4]), chunk=int(misc[5]),
+                          attn_k=int(g["idx"].shape[-1]), mlp_k=int(gb["ks"][1]))
+    blk = ops.Block(cfg, {k[2:]: g[k] for k in g if k.startswith("w_")}, production=False)
+    idx, cnt = g["idx"], g["counts"]
+    st = index_set(ops, idx, cnt, cfg.chunk, n)
+    for t, dense in enumerate(g["sched"]):
+        y = blk.step(T(g[f"x{t}"]), bool(dense), static=st if dense else None)
+        assert np.array_equal(N(y), g[f"y{t}"]), t
+        ai, ac = blk.indices(False)
+        assert np.array_equal(N(ac), cnt), t
+        for ii in np.ndindex(*cnt.shape):
+            assert np.array_equal(N(ai)[ii][:cnt[ii]], idx[ii][:cnt[ii]]), (t, ii)
+
+
+def test_prod_block_static_pattern_vs_check(ops, port):
+    """The same static-pattern semantics in PROD (cfg1-like shapes, ragged counts with empty
+    chunks), against CHECK mode on identical bf16-rounded inputs."""
+    n, d, h, e, f, c = 1024, 768, 12, 64, 3072, 64
+    ak, mk = 102, 307
+    std = 1 / np.sqrt(d)
+    w = {"wq": port.gaussian(21, (d, d), std), "wk": port.gaussian(22, (d, d), std),
+         "wv": port.gaussian(23, (d, d), std), "wo": port.gaussian(24, (d, d), std / 2),
+         "w1": port.gaussian(25, (f, d), std), "b1": port.gaussian(26, (f,), std),
+         "w2": port.gaussian(27, (f, d), std / 2), "b2": port.gaussian(28, (d,), std / 2)}
+    w = {k: bf(v) if k not in ("b1", "b2") else v for k, v in w.items()}
+    cfg = ops.BlockConfig(batch=1, seq=n, dim=d, heads=h, head_dim=e, hidden=f, chunk=c,
+                          attn_k=ak, mlp_k=mk)
+    rng = np.random.default_rng(459)
+    nc = n // c
+    idx = np.zeros((1, h, nc, ak), np.int32)
+    cnt = rng.integers(0, ak + 1, size=(1, h, nc)).astype(np.int32)
+    cnt[0, 0, :3] = 0  # empty chunks pass the cached residual through
+    for ii in np.ndindex(1, h, nc):
+        idx[ii][:cnt[ii]] = rng.permutation(n)[:cnt[ii]]
+    st = index_set(ops, idx, cnt, c, n)
+    prod = ops.Block(cfg, w, production=True)
+    chk = ops.Block(cfg, w, production=False)
+    x0 = port.gaussian(2300, (1, n, d))
+    for t, dense in enumerate([1, 0, 0, 1, 0]):
+        x = bf(x0 + 0.02 * t * port.gaussian(4100 + t, x0.shape))
+        yp = prod.step(T(x, torch.bfloat16), bool(dense), static=st if dense else None)
+        yc = chk.step(T(x), bool(dense), static=st if dense else None)
+        err = rel_l2(N(yp) - x, N(yc) - x)
+        assert err < REL_L2_TOL, (t, err)
+        _, pc = prod.indices(False)
+        assert np.array_equal(N(pc), cnt), t
