@@ -200,6 +200,28 @@ def test_check_attention_errors(ops, port):
     cache = ops.AttentionCache()
     with pytest.raises(errors.StateError):
         ops.attention_step(q, q, q, cache, False, 2, 4)
+    # non-finite logits: softmax_rows raises NumericError (tensor.cpp:122-125)
+    qn = q.clone()
+    qn[0, 0, 3, 1] = float("inf")
+    with pytest.raises(errors.NumericError):
+        ops.dense_attention(qn, q, q)
+    qn[0, 0, 3, 1] = float("nan")
+    with pytest.raises(errors.NumericError):
+        ops.column_sum_attention(qn, q, q, None, 4)
+    # the context is usable again afterwards
+    assert torch.isfinite(ops.dense_attention(q, q, q)).all()
+
+
+def test_block_sparse_before_dense_is_state_error(ops, golden):
+    """model_forward_step: a sparse step before any dense step throws StateError
+    (attention.cpp:196-219) in both modes; the block stays usable."""
+    from paper_2506_03275_b200 import errors
+    g = golden("block")
+    blk = _golden_block(ops, g, production=False)
+    with pytest.raises(errors.StateError):
+        blk.step(T(g["x0"]), False)
+    y = blk.step(T(g["x0"]), True)
+    assert np.array_equal(N(y), g["y0"])
 
 
 # ------------------------------------------------------------------ CHECK-mode MLP
