@@ -98,6 +98,7 @@ struct AttnParams {
     float* colsum;
     int layout;
     int heads, n, chunk, chunks, items;
+    int cs_chunk, cs_chunks;  // colsum chunking when it differs from the item rows (else 0)
     float qk_scale_log2;  // log2(e) / sqrt(E)
 };
 
@@ -583,13 +584,36 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 if (do_cs) {
                     named_bar_sync(1, 256);
                     const int st = sw * 32 + lane;
-                    if (st < 128 && st < ncols) {
+                    if (st < 128 && st < ncols && p.cs_chunk == 0) {
                         float s = 0.f;
                         for (int t = 0; t < NT; ++t)
                             for (int qd = 0; qd < 4; ++qd)
                                 if (t * 128 + qd * 32 < p.chunk)
                                     s += cs_part[(((g & 1) * NT + t) * 4 + qd) * 128 + st];
                         p.colsum[((int64_t)bh * p.chunks + c) * p.n + j * 128 + st] = s;
+                    } else if (st < 128 && st < ncols) {
+                        // item rows != colsum chunk (256-row items over, e.g., 192-row chunks):
+                        // every 32-row quadrant lies in one chunk and an item touches at most
+                        // two; each (chunk, key) gets at most two atomic adds onto a zeroed
+                        // output, so the sum is order-independent (a + b == b + a)
+                        const int64_t r0 = (int64_t)c * p.chunk;
+                        const int64_t c_lo = r0 / p.cs_chunk;
+                        float s_lo = 0.f, s_hi = 0.f;
+                        bool hi = false;
+                        for (int t = 0; t < NT; ++t)
+                            for (int qd = 0; qd < 4; ++qd)
+                                if (t * 128 + qd * 32 < p.chunk) {
+                                    const float vv = cs_part[(((g & 1) * NT + t) * 4 + qd) * 128 + st];
+                                    if ((r0 + t * 128 + qd * 32) / p.cs_chunk == c_lo) {
+                                        s_lo += vv;
+                                    } else {
+                                        s_hi += vv;
+                                        hi = true;
+                                    }
+                                }
+                        float* cs0 = p.colsum + ((int64_t)bh * p.cs_chunks + c_lo) * p.n + j * 128 + st;
+                        atomicAdd(cs0, s_lo);
+                        if (hi) atomicAdd(cs0 + p.n, s_hi);
                     }
                 }
             }
@@ -800,6 +824,8 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
     p.n = (int)a.n;
     p.chunk = (int)a.chunk;
     p.chunks = (int)(a.n / a.chunk);
+    p.cs_chunk = (a.colsum != nullptr && a.cs_chunk > 0 && a.cs_chunk != a.chunk) ? (int)a.cs_chunk : 0;
+    p.cs_chunks = p.cs_chunk ? (int)(a.n / a.cs_chunk) : 0;
     p.items = (int)(a.batch * a.heads * p.chunks);
     p.qk_scale_log2 = kLog2e / std::sqrt((float)E);
 

@@ -93,6 +93,10 @@ struct AttnTcArgs {
     float* colsum;     // nullable [B,H,N/c,N]
     int layout;
     int64_t batch, heads, n, e, chunk;
+    // colsum chunk when the work items use a different row count (chunk = item rows; the
+    // column sums are per cs_chunk rows, accumulated atomically into a zeroed colsum);
+    // 0 = the item rows
+    int64_t cs_chunk;
 };
 // Returns cudaErrorNotSupported for shapes outside the envelope.
 cudaError_t attn_tc(const AttnTcArgs& a, cudaStream_t s);

@@ -307,8 +307,11 @@ def test_prod_sparse_delta_attention(ops, port, e, chunk, n, layout, h):
                     assert np.array_equal(got[0, hh, c * chunk:(c + 1) * chunk], to_bhne(b16)[0, hh, c * chunk:(c + 1) * chunk])
 
 
+# (192, 768) / (192, 1536) / (128, 1024): 256-row work items with per-chunk column sums merged
+# across items (capi_ops.cpp); the others run one chunk per item
 @pytest.mark.parametrize("e,chunk,n,h", [(128, 192, 768, 2), (64, 64, 512, 2), (128, 128, 384, 2),
-                                         (64, 64, 1024, 10)])
+                                         (64, 64, 1024, 10), (128, 192, 1536, 2),
+                                         (128, 128, 1024, 3)])
 def test_prod_dense_and_colsum_attention(ops, port, e, chunk, n, h):
     q, k, v = (bf(port.gaussian(400 + i, (1, h, n, e))) for i in range(3))
     want_o, want_cs, (wm, wl) = port.column_sum_attention(q, k, v, None, chunk)
