@@ -163,7 +163,8 @@ class Generation:
     def prepare(self, scale: float):
         """PROD: run each step kind once eagerly (workspaces, tensor maps, cuBLAS plans), then
         record one CUDA graph per kind.  The block caches this touches are rebuilt by the
-        run's first step, which is always dense (schedule.cpp:21-41)."""
+        run's first step, which is always dense (schedule.cpp:21-41); run() starts the
+        warm-up from the run's own x0 so the stale softmax stats equal fresh ones."""
         for mode in (DENSE, SPARSE, SKIPPED):
             self._step(mode, scale)
         torch.cuda.synchronize()
@@ -179,11 +180,18 @@ class Generation:
         scale = float(np.float32(1.0) / np.float32(total))  # harness.cpp:149, fp32 division
         x0, _ = ops.voxel_order(grid0.to(torch.float32).contiguous(), self.layout)
         base = self._dense_trajectory(x0, total, scale) if self.baseline else None
+
+        def reset():
+            self.latent.copy_(x0)
+            if self.prod:
+                self.shadow.copy_(x0.to(torch.bfloat16))
         if self.use_graphs:
+            # warm-up from x0 itself: its dense step leaves exactly the softmax stats the
+            # reference's first dense step computes fresh (attention.cpp:122-137), which the
+            # captured dense step then reads as its "previous" stats
+            reset()
             self.prepare(scale)
-        self.latent.copy_(x0)
-        if self.prod:
-            self.shadow.copy_(x0.to(torch.bfloat16))
+        reset()
         snaps = [torch.empty_like(self.latent) for _ in modes] if base is not None else None
         rep = RunReport(modes=modes)
         stream = torch.cuda.current_stream()
