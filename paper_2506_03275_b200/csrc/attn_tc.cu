@@ -549,20 +549,28 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                             for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(pv[2 * q], pv[2 * q + 1]);
                             tmem_st16(tS + hf * 32 + cc * 16, pk);
                             if (do_cs) {
-                                // transpose-reduce the warp's 32x32 block: lane ends with column `lane`
+                                // transpose-reduce the warp's 32 x 32 block of w * p on packed
+                                // f16 column pairs (16 shuffles instead of 31; the sums only
+                                // rank keys for the top-k): after the rounds over lane bits
+                                // 4..1 lane l holds columns (l & ~1, l | 1) over half the
+                                // lanes, the last exchange adds the other half
+                                uint32_t hp[16];
+                                const float2 w2 = make_float2(w, w);
 #pragma unroll
-                                for (int i = 0; i < 32; ++i) pv[i] *= w;
+                                for (int q = 0; q < 16; ++q)
+                                    hp[q] = pack_f16x2(__fmul2_rn(make_float2(pv[2 * q], pv[2 * q + 1]), w2));
 #pragma unroll
-                                for (int wd = 16; wd >= 1; wd >>= 1) {
+                                for (int wd = 16, hw = 8; wd >= 2; wd >>= 1, hw >>= 1) {
                                     const bool upper = (lane & wd) != 0;
 #pragma unroll
-                                    for (int i = 0; i < wd; ++i) {
-                                        const float send = upper ? pv[i] : pv[i + wd];
-                                        const float keep = upper ? pv[i + wd] : pv[i];
-                                        pv[i] = keep + __shfl_xor_sync(0xffffffffu, send, wd);
+                                    for (int i = 0; i < hw; ++i) {
+                                        const uint32_t send = upper ? hp[i] : hp[i + hw];
+                                        const uint32_t keep = upper ? hp[i + hw] : hp[i];
+                                        hp[i] = hadd2_u32(keep, __shfl_xor_sync(0xffffffffu, send, wd));
                                     }
                                 }
-                                csp[lane] = pv[0];
+                                const float2 tot = unpack_f16x2(hadd2_u32(hp[0], __shfl_xor_sync(0xffffffffu, hp[0], 1)));
+                                csp[lane] = (lane & 1) ? tot.y : tot.x;
                             }
                         }
                         const float2 part = __fadd2_rn(part0, part1);
