@@ -26,12 +26,22 @@ def main():
     ap.add_argument("--n", type=int, default=4608)
     ap.add_argument("--blocks", type=int, default=12)
     ap.add_argument("--cta", type=int, default=0)
+    ap.add_argument("--colsum", type=int, default=0, help="column-sum chunk (0: plain dense)")
     args = ap.parse_args()
     g = torch.Generator(device="cuda").manual_seed(7)
     q, k, v = (torch.randn((1, args.n, args.heads, 128), device="cuda", generator=g).to(torch.bfloat16)
                for _ in range(3))
+    stats = None
+    if args.colsum:
+        r0 = ops.column_sum_attention(q, k, v, None, args.colsum, layout=1)
+        stats = r0.stats
+
+    def launch():
+        if args.colsum:
+            return ops.column_sum_attention(q, k, v, stats, args.colsum, layout=1)
+        return ops.dense_attention(q, k, v, layout=1)
     for _ in range(3):
-        ops.dense_attention(q, k, v, layout=1)
+        launch()
     lib = _capi.lib()
     fn = lib.csd_debug_set_attn_trace
     fn.argtypes = [ctypes.c_void_p]
@@ -40,7 +50,7 @@ def main():
     fn(buf.data_ptr())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    ops.dense_attention(q, k, v, layout=1)
+    launch()
     e1.record()
     torch.cuda.synchronize()
     fn(None)
