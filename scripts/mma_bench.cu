@@ -21,6 +21,10 @@ using namespace csd::tc;
 // mode 6: mode 5 while 8 other warps run an ex2 / FFMA loop (softmax-like ALU load)
 // mode 7: mode 5 while 8 other warps run an FFMA-only loop
 // mode 8: mode 5 while 8 other warps run shuffles
+// mode 9: mode 0 (SS, smem-bandwidth-bound) while 8 warps stream 16-byte smem stores
+// mode 10: mode 1 (TS) while 8 warps stream 16-byte smem stores
+// mode 11: mode 5 while 8 warps stream TMEM loads + stores on other columns (softmax-like)
+// mode 12: mode 5 while 8 warps load / store the columns the MMAs use (as the softmax does)
 template <int MODE>
 __global__ void __launch_bounds__(384, 1) k_mma_rate(long long* out, int groups) {
     extern __shared__ uint8_t smem_raw[];
@@ -60,7 +64,7 @@ __global__ void __launch_bounds__(384, 1) k_mma_rate(long long* out, int groups)
         __syncwarp();
         t0 = clock64();
         for (int g = 0; g < groups; ++g) {
-            const bool pv = MODE == 1 || (MODE >= 5 && (g & 1));
+            const bool pv = MODE == 1 || MODE == 10 || ((MODE >= 5 && MODE <= 8 || MODE >= 11) && (g & 1));
             if (elect_one()) {
                 if (pv) {
 #pragma unroll
@@ -81,6 +85,34 @@ __global__ void __launch_bounds__(384, 1) k_mma_rate(long long* out, int groups)
         mbar_wait(&bar, 0);
         t1 = clock64();
         if (lane == 0) stop = 1;
+    } else if (warp >= 4 && MODE >= 11) {
+        const uint32_t col = MODE == 11 ? 128u + (warp >> 2) * 64u : (uint32_t)(warp >> 2) * 64u;
+        const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + col;
+        uint32_t acc = 0;
+        while (!stop) {
+            uint32_t r[32];
+            tmem_ld32(ta, r);
+            tmem_ld_wait();
+            uint32_t pk[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) pk[q] = r[2 * q] ^ r[2 * q + 1];
+            if (MODE == 11) tmem_st16(ta + 32, pk);
+            tmem_st_wait();
+            acc ^= pk[3];
+        }
+        if (acc == 77u) out[1] = 1;
+    } else if (warp >= 4 && MODE >= 9) {
+        // smem write stream into the region past the operands (96 KB .. 160 KB)
+        uint4* dst = reinterpret_cast<uint4*>(smem + 96 * 1024);
+        const uint4 v = make_uint4(threadIdx.x, 1u, 2u, 3u);
+        int i = threadIdx.x - 128;
+        while (!stop) {
+#pragma unroll 8
+            for (int r = 0; r < 64; ++r) {
+                dst[i] = v;
+                i = (i + 256) & 4095;
+            }
+        }
     } else if (warp >= 4 && MODE >= 6) {
         float a = 0.001f * threadIdx.x, b = 1.0001f, c2 = 0.5f;
         uint32_t u = threadIdx.x;
@@ -110,7 +142,7 @@ __global__ void __launch_bounds__(384, 1) k_mma_rate(long long* out, int groups)
 template <int MODE>
 static void run(const char* name, long long* d, double flop_per_instr) {
     const int groups = 2000;
-    const int smem = 96 * 1024 + 1024;
+    const int smem = 160 * 1024 + 1024;
     cudaFuncSetAttribute(k_mma_rate<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     for (int rep = 0; rep < 2; ++rep) k_mma_rate<MODE><<<148, 384, smem>>>(d, groups);
     long long h = 0;
@@ -134,6 +166,10 @@ int main() {
     run<6>("  ... + 8 warps ex2/FFMA loop", d, f128);
     run<7>("  ... + 8 warps FFMA loop", d, f128);
     run<8>("  ... + 8 warps shuffle loop", d, f128);
+    run<9>("SS + 8 warps streaming smem stores", d, f128);
+    run<10>("TS + 8 warps streaming smem stores", d, f128);
+    run<11>("S/PV + 8 warps TMEM ld/st on other columns", d, f128);
+    run<12>("S/PV + 8 warps TMEM loads of the MMA columns", d, f128);
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
