@@ -41,9 +41,11 @@ using namespace csd::tc;
 
 // Debug timeline (scripts/attn_trace.py): when set, CTAs < kTraceCtas record SM clock64()
 // stamps at fixed slots (start, Q / K / V issue, S issue, softmax and epilogue phases).
+// The buffers travel in the kernel parameters (constant bank): an untraced launch pays a
+// uniform predicate per trace point, not a global load on the softmax's critical path.
 constexpr int kTraceCtas = 8, kTraceSlots = 1024;
-__device__ uint64_t* g_attn_trace = nullptr;
-__device__ uint64_t* g_attn_span = nullptr;  // [grid][2] globaltimer at CTA start / end
+static uint64_t* h_attn_trace = nullptr;  // host-side settings (csd_debug_set_attn_*)
+static uint64_t* h_attn_span = nullptr;
 __device__ __forceinline__ uint64_t globaltimer_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -51,7 +53,7 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 #define ATTN_TRACE(slot)                                                                  \
     do {                                                                                  \
-        uint64_t* tr_ = g_attn_trace;                                                     \
+        uint64_t* tr_ = p.trace;                                                          \
         if (tr_ != nullptr && blockIdx.x < kTraceCtas && (slot) < kTraceSlots)            \
             tr_[blockIdx.x * kTraceSlots + (slot)] = clock64();                           \
     } while (0)
@@ -99,6 +101,8 @@ struct AttnParams {
     int layout;
     int heads, n, chunk, chunks, items;
     int cs_chunk, cs_chunks;  // colsum chunking when it differs from the item rows (else 0)
+    uint64_t* trace;          // debug timeline (null: off)
+    uint64_t* span;           // debug per-CTA [start, end] globaltimer (null: off)
     float qk_scale_log2;  // log2(e) / sqrt(E)
 };
 
@@ -126,7 +130,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     const bool dense = p.idx == nullptr;
     const int items = p.items;
     if (threadIdx.x == 0) ATTN_TRACE(0);
-    if (threadIdx.x == 0 && g_attn_span != nullptr) g_attn_span[2 * blockIdx.x] = globaltimer_ns();
+    if (threadIdx.x == 0 && p.span != nullptr) p.span[2 * blockIdx.x] = globaltimer_ns();
 
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
     uint64_t* bar_q = bars + 0;
@@ -758,7 +762,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     }
     tc_fence_before();
     __syncthreads();
-    if (threadIdx.x == 0 && g_attn_span != nullptr) g_attn_span[2 * blockIdx.x + 1] = globaltimer_ns();
+    if (threadIdx.x == 0 && p.span != nullptr) p.span[2 * blockIdx.x + 1] = globaltimer_ns();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<L::kTmemCols>(tmem);
@@ -832,6 +836,8 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
     p.n = (int)a.n;
     p.chunk = (int)a.chunk;
     p.chunks = (int)(a.n / a.chunk);
+    p.trace = h_attn_trace;
+    p.span = h_attn_span;
     p.cs_chunk = (a.colsum != nullptr && a.cs_chunk > 0 && a.cs_chunk != a.chunk) ? (int)a.cs_chunk : 0;
     p.cs_chunks = p.cs_chunk ? (int)(a.n / a.cs_chunk) : 0;
     p.items = (int)(a.batch * a.heads * p.chunks);
@@ -900,10 +906,12 @@ cudaError_t attn_tc(const AttnTcArgs& a, cudaStream_t s) {
 // device array of kTraceCtas * kTraceSlots uint64 (nullptr disables tracing).
 extern "C" int csd_debug_set_attn_trace(void* dev_buf) {
     uint64_t* p = static_cast<uint64_t*>(dev_buf);
-    return cudaMemcpyToSymbol(csd::dev::g_attn_trace, &p, sizeof(p)) == cudaSuccess ? 0 : 7;
+    csd::dev::h_attn_trace = p;
+    return 0;
 }
 // Debug only: per-CTA [start, end] globaltimer stamps (2 x grid uint64).
 extern "C" int csd_debug_set_attn_span(void* dev_buf) {
     uint64_t* p = static_cast<uint64_t*>(dev_buf);
-    return cudaMemcpyToSymbol(csd::dev::g_attn_span, &p, sizeof(p)) == cudaSuccess ? 0 : 7;
+    csd::dev::h_attn_span = p;
+    return 0;
 }
