@@ -32,10 +32,11 @@ bool make_map_bf16(CUtensorMap* m, const void* base, uint64_t cols, uint64_t row
 
 // Debug timeline (scripts/mlp_trace.py): CTAs with blockIdx.y == 0 and blockIdx.x < 8
 // record clock64() at fixed slots when the pointer is set.
-__device__ uint64_t* g_mlp_trace = nullptr;
+// debug timeline buffer: host setting, passed in the kernel parameters (constant bank)
+static uint64_t* h_mlp_trace = nullptr;
 #define MLP_TRACE(slot)                                                                   \
     do {                                                                                  \
-        uint64_t* tr_ = g_mlp_trace;                                                      \
+        uint64_t* tr_ = p.trace;                                                          \
         if (tr_ != nullptr && blockIdx.y == 0 && blockIdx.x < 8 && (slot) < 256)          \
             tr_[blockIdx.x * 256 + (slot)] = clock64();                                   \
     } while (0)
@@ -55,6 +56,7 @@ struct MlpLayout {
 };
 
 struct MlpParams {
+    uint64_t* trace;  // debug timeline (null: off)
     const __nv_bfloat16* w1;  // gathered rows are staged with cp.async from these
     const __nv_bfloat16* w2;
     const int32_t* idx;
@@ -621,6 +623,7 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
         !make_map_bf16(&tdl, delta_ws, k_pad, batch * nc * chunk, k_pad, 64))
         return cudaErrorInvalidValue;
     MlpParams p{};
+    p.trace = h_mlp_trace;
     p.w1 = (const __nv_bfloat16*)w1;
     p.w2 = (const __nv_bfloat16*)w2;
     p.idx = idx;
@@ -714,5 +717,6 @@ cudaError_t prod_sparse_delta_mlp_tc(const void* x, const void* w1, const float*
 // Debug only (scripts/mlp_trace.py): timeline buffer of 8 x 256 uint64 for k_smlp_up.
 extern "C" int csd_debug_set_mlp_trace(void* dev_buf) {
     uint64_t* p = static_cast<uint64_t*>(dev_buf);
-    return cudaMemcpyToSymbol(csd::dev::g_mlp_trace, &p, sizeof(p)) == cudaSuccess ? 0 : 7;
+    csd::dev::h_mlp_trace = p;
+    return 0;
 }

@@ -24,8 +24,10 @@ namespace dev {
 __device__ uint64_t* g_topk_trace = nullptr;
 #define TOPK_TRACE(slot)                                                                  \
     do {                                                                                  \
-        uint64_t* tr_ = g_topk_trace;                                                     \
-        if (tr_ != nullptr && blockIdx.x == 0 && threadIdx.x == 0) tr_[slot] = clock64();  \
+        if (blockIdx.x == 0 && threadIdx.x == 0) { /* one thread pays the pointer load */ \
+            uint64_t* tr_ = g_topk_trace;                                                 \
+            if (tr_ != nullptr) tr_[slot] = clock64();                                    \
+        }                                                                                 \
     } while (0)
 
 constexpr int kTopkThreads = 512;
