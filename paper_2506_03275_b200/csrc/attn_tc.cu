@@ -630,21 +630,22 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 }
             }
             // ------------------------------------------------------------ epilogue
-            // full row sums: the halves swap partial sums (the first barrier retires the last
-            // block's max exchange, the third this exchange before the next item reuses xch)
+            // full row sums: the halves swap partial sums for all tiles at once (the first
+            // barrier retires the last block's max exchange, the third this exchange before
+            // the next item reuses xch)
             float l_full[NT];
+            named_bar_sync(qbar, 64);
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
                 l_full[t] = l_run[t];
-                if (t * 128 + quad * 32 < p.chunk) {
-                    float* xr = xch + (t * 128 + quad * 32 + lane) * 2;
-                    named_bar_sync(qbar, 64);
-                    xr[hf] = l_run[t];
-                    named_bar_sync(qbar, 64);
-                    l_full[t] = l_run[t] + xr[hf ^ 1];
-                    named_bar_sync(qbar, 64);
-                }
+                if (t * 128 + quad * 32 < p.chunk) xch[(t * 128 + quad * 32 + lane) * 2 + hf] = l_run[t];
             }
+            named_bar_sync(qbar, 64);
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+                if (t * 128 + quad * 32 < p.chunk)
+                    l_full[t] = l_run[t] + xch[(t * 128 + quad * 32 + lane) * 2 + (hf ^ 1)];
+            named_bar_sync(qbar, 64);
             const bool has_base = p.base != nullptr;
             if (p.stage_base) {
                 // out = base + scale * O / l (north_star item 5) with the item's base tile
