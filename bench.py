@@ -329,12 +329,16 @@ def run_ours(args, rank, world):
                                 "profiles/latest_full.json)",
                 "alg_bytes": att["alg_bytes"],
                 "tensor_frac": round(att["flops"] / (att["ms"] * 1e-3) / 1e12 / tf, 4),
-                # the binding staging path: gathered K/V row pieces through TMA tile::gather4,
-                # whose per-SM rate (14 B/ns, scripts/gather_bench2.cu) caps the kernel
+                # the K/V rows gathered through TMA tile::gather4 (14 B/ns per SM in isolation,
+                # scripts/gather_bench2.cu).  Not the binding resource: a compacted-rows variant
+                # with plain TMA tiles was no faster; the kernel is bound by its
+                # softmax -> P.V -> S schedule at ~47 % tensor-pipe occupancy per block, the
+                # tcgen05.mma itself running at 64 cycles per M128.N128.K16 (scripts/mma_bench.cu)
                 "gather": {"bytes": att["gather_bytes"],
                            "achieved_gbs": round(att["gather_bytes"] / (att["ms"] * 1e-3) / 1e9, 1),
                            "measured_gather4_gbs": 148 * 14.0,
                            "frac": round(att["gather_bytes"] / (att["ms"] * 1e-3) / 1e9 / (148 * 14.0), 4)},
+                "limiter": "softmax -> P.V -> S dependency chain per key block (not HBM, not gather4)",
             },
         }
     return out
