@@ -396,7 +396,9 @@ struct DnLayout {
     static constexpr uint32_t kStgBytes = 4 * NT * 4096;     // one 32 x 32 fp32 block per warp
     static constexpr uint32_t kBar = kStg + kStgBytes;
     static constexpr uint32_t kAlloc = kBar + 256 + 1024;
-    static constexpr uint32_t kThreads = 128 + 128 * NT;
+    // warps 0 (TMA + copy), 1 (MMA), 2-3 (copy), 4 .. 4 + 4 NT - 1 (epilogue), then 4 more
+    // copy warps: the W2 row gather (cp.async, LSU rate per issuing warp) is the K loop's limiter
+    static constexpr uint32_t kThreads = 256 + 128 * NT;
     static constexpr uint32_t kTmemCols = 2 * NT * 128 <= 256 ? 256 : 512;
 };
 
@@ -416,7 +418,8 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
     uint64_t* tfull = bars + 2 * kDnStages;   // [2] accumulator buffer final
     uint64_t* tempty = tfull + 2;             // [2] accumulator buffer drained
     uint32_t* slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    constexpr int kCopyThreads = 96;          // warps 0, 2, 3
+    constexpr int kCopyThreads = 224;         // warps 0, 2, 3 and the 4 trailing warps
+    constexpr int kXtra = 4 + 4 * NT;         // first trailing copy warp
     if (threadIdx.x == 0) {
         if (blockIdx.x == 0) MLP_TRACE(200);
         for (int s = 0; s < kDnStages; ++s) {
@@ -436,10 +439,11 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
     const uint32_t tmem = *slot;
     auto kblocks_of = [&](int item) { return (p.counts[item / ntd] + 63) / 64; };
 
-    if (warp == 0 || warp == 2 || warp == 3) {
-        // producers: warp 0 lane 0 the delta tiles (TMA); all 96 threads the W2 k-slices,
+    if (warp == 0 || warp == 2 || warp == 3 || warp >= kXtra) {
+        // producers: warp 0 lane 0 the delta tiles (TMA); all 224 threads the W2 k-slices,
         // one row's 16 pieces (2 strips x 8) on consecutive threads
-        const int ct = warp == 0 ? lane : (warp - 1) * 32 + lane;
+        if constexpr (NT == 2) regs_dec<72>();  // 512 threads: the epilogue gets the registers
+        const int ct = warp == 0 ? lane : warp < 4 ? (warp - 1) * 32 + lane : 96 + (warp - kXtra) * 32 + lane;
         constexpr int kPer = (64 * 16 + kCopyThreads - 1) / kCopyThreads;
         if (warp == 0 && lane == 0) tma_prefetch_desc(&tm_delta);
         const uint32_t s0 = smem_u32(smem);
@@ -481,6 +485,7 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
             }
         }
     } else if (warp == 1) {
+        if constexpr (NT == 2) regs_dec<72>();
         if (lane == 0) {
             constexpr uint32_t id = idesc_bf16(128, 128, false, true);
             const uint32_t s0 = smem_u32(smem);
@@ -515,6 +520,7 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
             }
         }
     } else {
+        if constexpr (NT == 2) regs_inc<184>();
         // epilogue warps: thread = chunk row for the TMEM read; each warp then transposes
         // 32 x 32 fp32 blocks through its own smem slice so the M_cache read-modify-write and
         // the residual run row-contiguously (8 lanes x 16 B per 32-column row segment)
