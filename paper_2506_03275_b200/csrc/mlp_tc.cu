@@ -520,6 +520,8 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
             }
         }
     } else {
+        // setmaxnreg.inc draws only on registers this CTA's decs released (8 warps x 56 at
+        // 128 -> 72 fund exactly 8 warps x 56 at 128 -> 184); asking for more deadlocks
         if constexpr (NT == 2) regs_inc<184>();
         // epilogue warps: thread = chunk row for the TMEM read; each warp then transposes
         // 32 x 32 fp32 blocks through its own smem slice so the M_cache read-modify-write and
