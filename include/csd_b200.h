@@ -235,11 +235,17 @@ csd_status csd_block_create(csd_ctx* ctx, csd_mode mode, const csd_block_config*
                             const float* w1, const float* b1, const float* w2, const float* b2,
                             csd_block** out);
 csd_status csd_block_destroy(csd_block* blk);
+/* Forget every cache (a fresh ModelState, model.cpp:101-105): the next step must be dense
+ * and computes its column sums with fresh softmax stats. */
+csd_status csd_block_reset(csd_block* blk);
 /* model_forward_step for one layer: x_out = block(x_in).  x in the mode's
  * activation dtype, [B,N,D] device.  dense != 0 refreshes the caches.
  * static_idx/static_counts (nullable, device) replace the attention top-k
- * on dense steps (attention.hpp:50-52).  A sparse step before any dense step
- * returns CSD_ERR_STATE. */
+ * on dense steps (attention.hpp:50-52): int32 [B, heads_local, N/chunk, static_k_max]
+ * and [B, heads_local, N/chunk], static_k_max == cfg.attn_k.  The pattern is validated
+ * before anything runs (CSD_ERR_SHAPE / CSD_ERR_INDEX / CSD_ERR_VALUE leave every cache
+ * untouched; synchronous unless the stream is capturing, then reported by csd_ctx_sync).
+ * A sparse step before any dense step returns CSD_ERR_STATE. */
 csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int dense,
                           const int32_t* static_idx, const int32_t* static_counts,
                           int64_t static_k_max, void* stream);

@@ -67,6 +67,7 @@ SIGNATURES = {
     "csd_add": (i32, [p, i32, fp, fp, i64, fp, p]),
     "csd_block_create": (i32, [p, i32, C.POINTER(BlockConfig)] + [fp] * 8 + [C.POINTER(p)]),
     "csd_block_destroy": (i32, [p]),
+    "csd_block_reset": (i32, [p]),
     "csd_block_step": (i32, [p, fp, fp, C.c_int, fp, fp, i64, p]),
     "csd_block_cache": (i32, [p, C.c_int, fp, fp, p]),
     "csd_block_attn_partial": (i32, [p, fp, C.c_int, fp, p]),

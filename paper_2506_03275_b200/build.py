@@ -93,15 +93,6 @@ HOST_SRC = os.path.join(PKG, "host", "csd_host.cpp")
 HOST_LIB = os.path.join(PKG, "libcsd_host.so")
 
 
-def _json_include():
-    import site
-    for sp in site.getsitepackages():
-        d = os.path.join(sp, "include", "cudnn_frontend", "thirdparty", "nlohmann")
-        if os.path.exists(os.path.join(d, "json.hpp")):
-            return d
-    raise RuntimeError("nlohmann/json.hpp not found (cudnn_frontend third-party headers)")
-
-
 def build_host(force: bool = False, verbose: bool = False) -> str:
     """libcsd_host.so: the reference's C++ csd:: API (include/csd/*.hpp) over the C ABI."""
     deps = [HOST_SRC, LIB] + [os.path.join(INCLUDE, "csd", f)
@@ -110,7 +101,7 @@ def build_host(force: bool = False, verbose: bool = False) -> str:
             and os.path.getmtime(HOST_LIB) >= max(os.path.getmtime(p) for p in deps)):
         return HOST_LIB
     cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-ffp-contract=off",
-           "-I", INCLUDE, "-I", _json_include(), "-o", HOST_LIB, HOST_SRC,
+           "-I", INCLUDE, "-o", HOST_LIB, HOST_SRC,
            "-L", PKG, "-l:libcsd_b200.so", "-Wl,-rpath,$ORIGIN"]
     if verbose:
         print(" ".join(cmd), flush=True)

@@ -32,6 +32,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "launch_util.h"
 #include "tc_common.cuh"
 
 namespace csd {
@@ -873,19 +874,11 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
     const uint32_t smem_bytes = p.off_bar + 256;
     if (smem_bytes > L::kMaxSmem) return cudaErrorNotSupported;
     auto kern = k_attn_tc<E, NT>;
-    static bool attr_done = false;  // once per instantiation (keeps graph capture clean)
-    if (!attr_done) {
-        cudaError_t err =
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kMaxSmem);
+    {
+        cudaError_t err = ensure_smem_attr(kern, (int)L::kMaxSmem);  // per device
         if (err != cudaSuccess) return err;
-        attr_done = true;
     }
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = sm_count();
     // persistent: one CTA per SM (smem-limited), items strided over the grid
     const unsigned grid = (unsigned)std::min<int64_t>(p.items, sms);
     kern<<<grid, L::kThreads, smem_bytes, s>>>(tq, tk, tv, tkg, tvg, tb, to, p);

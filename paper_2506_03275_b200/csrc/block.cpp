@@ -100,6 +100,7 @@ csd_status upload(csd_block* blk, void** dst, const float* host, int64_t rows, i
 
 static csd_status attn_core(csd_block* blk, const void* x_in, int dense, const int32_t* static_idx,
                             const int32_t* static_counts, int64_t static_k_max, void* stream);
+static csd_ctx* ctx_of(csd_block* blk) { return reinterpret_cast<csd_ctx*>(blk->ctx); }
 static csd_status sparse_mlp_apply(csd_block* blk, const void* x_mid, void* x_out, cudaStream_t s);
 
 extern "C" {
@@ -179,6 +180,16 @@ csd_status csd_block_create(csd_ctx* ctx, csd_mode mode, const csd_block_config*
     return CSD_OK;
 }
 
+csd_status csd_block_reset(csd_block* blk) {
+    // make_state (model.cpp:101-105): every cache empty again, so the next step must be
+    // dense and sees no stale softmax stats (fresh ones, attention.cpp:122-137)
+    if (!blk) return set_error(CSD_ERR_VALUE, "null block");
+    blk->attn_init = blk->mlp_init = false;
+    blk->attn_age = blk->mlp_age = 0;
+    blk->cur = 0;
+    return CSD_OK;
+}
+
 csd_status csd_block_destroy(csd_block* blk) {
     cudaDeviceSynchronize();
     delete blk;
@@ -195,6 +206,25 @@ csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int den
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (!dense && (!blk->attn_init || !blk->mlp_init))
         return set_error(CSD_ERR_STATE, "sparse attention step requested before any dense step");
+    if (dense && static_idx) {
+        // A caller-supplied static pattern (attention.cpp:205-213) is checked BEFORE anything
+        // runs, so a bad pattern leaves every cache untouched (as the reference, which throws
+        // before mutating the AttentionCache): k_max must be the block's, ids in [0, N)
+        // without duplicates, counts in [0, k_max].  Synchronous unless the stream is being
+        // captured (then the device flags surface at csd_ctx_sync).
+        if (!static_counts)
+            return set_error(CSD_ERR_VALUE, "static attention pattern without counts");
+        if (static_k_max != blk->a_kmax)
+            return set_error(CSD_ERR_SHAPE, "static pattern k_max %lld != block attn_k %lld",
+                             (long long)static_k_max, (long long)blk->a_kmax);
+        const cudaStream_t vs = static_cast<cudaStream_t>(stream);
+        const int64_t rows = c.batch * c.heads_local * (c.seq / c.chunk);
+        CSD_TRY(csd_validate_index_set(ctx_of(blk), static_idx, static_counts, rows, static_k_max,
+                                       c.seq, stream));
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(vs, &cs) != cudaSuccess || cs == cudaStreamCaptureStatusNone)
+            CSD_TRY(csd::check_flags(blk->ctx, vs));
+    }
     // PROD: the selected index sets feed order-invariant kernels -> skip the per-row sort
     struct SortGuard {
         Ctx* c;
@@ -265,8 +295,8 @@ static csd_status attn_core(csd_block* blk, const void* x_in, int dense, const i
     CSD_TRY(csd_project(ctx, md, x_in, blk->wq, B, N, D, Dl, blk->q, stream));
     CSD_TRY(csd_project(ctx, md, x_in, blk->wk, B, N, D, Dl, blk->k, stream));
     CSD_TRY(csd_project(ctx, md, x_in, blk->wv, B, N, D, Dl, blk->v, stream));
-    // Index sets produced inside the block are valid by construction (top-k);
-    // static patterns were validated when supplied.  Skip per-call validation.
+    // Index sets produced inside the block are valid by construction (top-k); a static
+    // pattern was validated by csd_block_step before anything ran.  Skip per-call validation.
     struct ValidateGuard {
         Ctx* c;
         bool old;
@@ -296,10 +326,6 @@ static csd_status attn_core(csd_block* blk, const void* x_in, int dense, const i
                                      stream));
         }
         if (static_idx) {  // keep a private copy (the cache owns its indices)
-            if (static_k_max != blk->a_kmax) {
-                return set_error(CSD_ERR_SHAPE, "static pattern k_max %lld != block attn_k %lld",
-                                 (long long)static_k_max, (long long)blk->a_kmax);
-            }
             CSD_CU(cudaMemcpyAsync(blk->aidx, static_idx, 4 * B * Hl * C * ukm,
                                    cudaMemcpyDeviceToDevice, s), "copy");
             CSD_CU(cudaMemcpyAsync(blk->acnt, static_counts, 4 * B * Hl * C,
@@ -330,7 +356,7 @@ static csd_status sparse_mlp_apply(csd_block* blk, const void* x_mid, void* x_ou
     if (!mlp_tc_supported(D, c.chunk))
         return set_error(CSD_ERR_UNSUPPORTED, "sparse-delta MLP envelope (D %% 128, chunk <= 256)");
     const int64_t k_pad = csd::dev::prod_smlp_delta_cols(mk, B * (N / c.chunk));
-    void* dws = blk->ctx->ws(csd::kWsDelta, 2 * B * N * k_pad);
+    void* dws = blk->ctx->ws(csd::kWsDelta, 2 * B * N * k_pad, s);
     if (!dws) return set_error(CSD_ERR_CUDA, "workspace allocation failed");
     CSD_CU(prod_sparse_delta_mlp_tc(x_mid, blk->w1, blk->b1, blk->w2, blk->midx, blk->mcnt, mk,
                                     c.chunk, B, N, D, Fl, blk->act, blk->mout, dws, s, x_mid, x_out),
@@ -383,10 +409,10 @@ csd_status csd_block_mlp_candidates(csd_block* blk, const void* x_mid, float* ca
     const int64_t B = c.batch, N = c.seq, D = c.dim, Fl = c.f_local, rows = B * (N / c.chunk);
     const int64_t k = c.mlp_k > 0 ? c.mlp_k : c.hidden;
     const int64_t k_loc = k < Fl ? k : Fl;
-    float* scores = (float*)blk->ctx->ws(csd::kWsScores, 4 * rows * Fl);
-    void* ws = blk->ctx->ws(csd::kWsMeans, prod_means_ws_bytes(B, N, D, Fl, c.chunk));
-    int32_t* ids = (int32_t*)blk->ctx->ws(csd::kWsIdx, 4 * rows * k_loc);
-    int32_t* cnt = (int32_t*)blk->ctx->ws(csd::kWsCounts, 4 * rows);
+    float* scores = (float*)blk->ctx->ws(csd::kWsScores, 4 * rows * Fl, s);
+    void* ws = blk->ctx->ws(csd::kWsMeans, prod_means_ws_bytes(B, N, D, Fl, c.chunk), s);
+    int32_t* ids = (int32_t*)blk->ctx->ws(csd::kWsIdx, 4 * rows * k_loc, s);
+    int32_t* cnt = (int32_t*)blk->ctx->ws(csd::kWsCounts, 4 * rows, s);
     if (!scores || !ws || !ids || !cnt) return set_error(CSD_ERR_CUDA, "workspace allocation failed");
     // local |T - T_m| (mlp.cpp:116) and the shard's top-k
     CSD_CU(prod_tile_means_tc(x_mid, blk->w1, B, N, D, Fl, c.chunk, blk->tmeans, scores, ws, s),
@@ -409,10 +435,10 @@ csd_status csd_block_mlp_sparse_partial(csd_block* blk, const void* x_mid,
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t B = c.batch, N = c.seq, D = c.dim, rows = B * (N / c.chunk);
     const int64_t k = c.mlp_k > 0 ? c.mlp_k : c.hidden;
-    float* ws_s = (float*)blk->ctx->ws(csd::kWsLogits, 4 * rows * world * k);
-    int32_t* ws_i = (int32_t*)blk->ctx->ws(csd::kWsProbs, 4 * rows * world * k);
-    int32_t* ws_p = (int32_t*)blk->ctx->ws(csd::kWsIdx, 4 * rows * k);
-    int32_t* ws_c = (int32_t*)blk->ctx->ws(csd::kWsCounts, 4 * rows);
+    float* ws_s = (float*)blk->ctx->ws(csd::kWsLogits, 4 * rows * world * k, s);
+    int32_t* ws_i = (int32_t*)blk->ctx->ws(csd::kWsProbs, 4 * rows * world * k, s);
+    int32_t* ws_p = (int32_t*)blk->ctx->ws(csd::kWsIdx, 4 * rows * k, s);
+    int32_t* ws_c = (int32_t*)blk->ctx->ws(csd::kWsCounts, 4 * rows, s);
     if (!ws_s || !ws_i || !ws_p || !ws_c) return set_error(CSD_ERR_CUDA, "workspace allocation failed");
     const int64_t mk = c.mlp_k > 0 ? c.mlp_k : c.f_local;  // row stride of midx
     CSD_CU(shard_merge(all_scores, all_ids, world, rows, k, c.f0, c.f_local, ws_s, ws_i, ws_p, ws_c,
@@ -449,7 +475,7 @@ csd_status csd_block_cache(csd_block* blk, int which, void* out, int32_t* counts
                     const char* src = (const char*)blk->resid + ((b * N) * Hl + h) * E * es;
                     float* dst = (float*)out + ((b * Hl + h) * N) * E;
                     if (blk->mode == CSD_MODE_PROD) {
-                        float* tmp = (float*)blk->ctx->ws(csd::kWsPre, 4 * N * Hl * E);
+                        float* tmp = (float*)blk->ctx->ws(csd::kWsPre, 4 * N * Hl * E, s);
                         CSD_CU(prod_cast_bf16_f32((const char*)blk->resid + b * N * Hl * E * es, tmp,
                                                   N * Hl * E, s), "cast");
                         CSD_CU(cudaMemcpy2DAsync(dst, E * 4, tmp + h * E, Hl * E * 4, E * 4, N,

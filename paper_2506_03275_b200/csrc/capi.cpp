@@ -40,15 +40,24 @@ csd_status cuda_status(cudaError_t e, const char* where) {
     return set_error(CSD_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 
-void* Ctx::ws(int slot, size_t bytes) {
+void* Ctx::ws(int slot, size_t bytes, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(mu);
     if (slot >= (int)bufs.size()) bufs.resize(slot + 1, {nullptr, 0});
     auto& b = bufs[slot];
     if (b.second < bytes) {
-        if (b.first) {
-            cudaStreamSynchronize(nullptr);
-            cudaDeviceSynchronize();
-            cudaFree(b.first);
+        // Growing during stream capture would put an allocation inside the captured region
+        // (and the new pointer would only be valid for this graph): refuse.
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (s != nullptr && cudaStreamIsCapturing(s, &cs) == cudaSuccess &&
+            cs != cudaStreamCaptureStatusNone) {
+            set_error(CSD_ERR_CUDA,
+                      "workspace slot %d must grow to %zu bytes during stream capture: run the "
+                      "step once eagerly before capturing it", slot, bytes);
+            return nullptr;
         }
+        // The old buffer is NOT freed: CUDA graphs captured earlier may still read and write
+        // it.  Retired buffers live until csd_ctx_destroy.
+        if (b.first) retired.push_back(b.first);
         b.first = nullptr;
         b.second = 0;
         if (cudaMalloc(&b.first, bytes < 256 ? 256 : bytes) != cudaSuccess) return nullptr;
@@ -183,6 +192,7 @@ csd_status csd_ctx_destroy(csd_ctx* ctx) {
     cudaDeviceSynchronize();
     for (auto& b : c->bufs)
         if (b.first) cudaFree(b.first);
+    for (void* p : c->retired) cudaFree(p);
     if (c->flags) cudaFree(c->flags);
     if (c->cublas) cublasDestroy(c->cublas);
     delete c;
@@ -248,7 +258,7 @@ csd_status csd_select_top_k(csd_ctx* ctx, const float* scores, int64_t rows, int
         CSD_CU(topk_rows(scores, rows, m, k, idx, counts, S(stream), c->sorted_topk), "topk_rows");
         c->launches += 1;
     } else {
-        void* ws = c->ws(csd::kWsTopk, sizeof(uint64_t) * rows * k);
+        void* ws = c->ws(csd::kWsTopk, sizeof(uint64_t) * rows * k, S(stream));
         if (!ws) return set_error(CSD_ERR_CUDA, "workspace allocation failed");
         CSD_CU(topk_rows_global(scores, rows, m, k, idx, counts, (uint64_t*)ws, S(stream)),
                "topk_rows_global");

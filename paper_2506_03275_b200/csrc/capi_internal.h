@@ -4,6 +4,7 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 
+#include <mutex>
 #include <utility>
 #include <vector>
 
@@ -35,6 +36,8 @@ struct Ctx {
     uint32_t* flags = nullptr;  // device error bits (kFlag*)
     cublasHandle_t cublas = nullptr;
     std::vector<std::pair<void*, size_t>> bufs;
+    std::vector<void*> retired;  // grown-out workspaces (graphs may still reference them)
+    std::mutex mu;
     int64_t launches = 0;          // our kernels launched through this context
     int64_t library_launches = 0;  // cuBLAS GEMM calls
     bool validate_prod = true;     // PROD-mode async index validation
@@ -44,7 +47,9 @@ struct Ctx {
     // skips the per-row sort.
     bool sorted_topk = true;
 
-    void* ws(int slot, size_t bytes);
+    // Workspace slot of at least `bytes`; `s` (the calling op's stream) lets a growth during
+    // stream capture fail loudly instead of allocating inside the capture.
+    void* ws(int slot, size_t bytes, cudaStream_t s = nullptr);
     cublasHandle_t blas();
 };
 

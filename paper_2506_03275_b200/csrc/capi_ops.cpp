@@ -85,15 +85,15 @@ csd_status prod_dense_mlp(Ctx* c, const void* x, const void* w1, const float* b1
     // chunk <= 256: GELU writes only the chunk-major cache and GEMM2 runs per chunk over it
     // (saves the [rows, F] row-major activation write); otherwise the row-major path
     const bool from_cm = chunk <= 256;
-    void* pre = c->ws(kWsPre, 2 * rows * f);
+    void* pre = c->ws(kWsPre, 2 * rows * f, s);
     CSD_TRY(need_ws(pre));
     void* act = nullptr;
     if (!from_cm) {
-        act = c->ws(kWsAct, 2 * rows * f);
+        act = c->ws(kWsAct, 2 * rows * f, s);
         CSD_TRY(need_ws(act));
     }
     if (!act_cm) {
-        act_cm = c->ws(kWsScores, 2 * rows * f);
+        act_cm = c->ws(kWsScores, 2 * rows * f, s);
         CSD_TRY(need_ws(act_cm));
     }
     CSD_TRY(gemm_bf16(c, x, w1, true, pre, false, rows, f, d, 0.0f, s));
@@ -145,8 +145,8 @@ csd_status csd_dense_attention(csd_ctx* ctx, csd_mode mode, csd_layout layout, c
         return prod_attn(c, a, s);
     }
     const int64_t bh = batch * heads;
-    float* L = (float*)c->ws(csd::kWsLogits, sizeof(float) * bh * n * n);
-    float* P = (float*)c->ws(csd::kWsProbs, sizeof(float) * bh * n * n);
+    float* L = (float*)c->ws(csd::kWsLogits, sizeof(float) * bh * n * n, s);
+    float* P = (float*)c->ws(csd::kWsProbs, sizeof(float) * bh * n * n, s);
     CSD_TRY(need_ws(L));
     CSD_TRY(need_ws(P));
     CSD_CU(check_attention_logits((const float*)q, (const float*)k, layout, batch, heads, n, e, n,
@@ -197,8 +197,8 @@ csd_status csd_column_sum_attention(csd_ctx* ctx, csd_mode mode, csd_layout layo
         return prod_attn(c, a, s);
     }
     const int64_t bh = batch * heads;
-    float* L = (float*)c->ws(csd::kWsLogits, sizeof(float) * bh * n * n);
-    float* P = (float*)c->ws(csd::kWsProbs, sizeof(float) * bh * n * n);
+    float* L = (float*)c->ws(csd::kWsLogits, sizeof(float) * bh * n * n, s);
+    float* P = (float*)c->ws(csd::kWsProbs, sizeof(float) * bh * n * n, s);
     CSD_TRY(need_ws(L));
     CSD_TRY(need_ws(P));
     CSD_CU(check_attention_logits((const float*)q, (const float*)k, layout, batch, heads, n, e, n,
@@ -243,7 +243,7 @@ csd_status csd_sparse_delta_attention(csd_ctx* ctx, csd_mode mode, csd_layout la
     const size_t bytes = sizeof(float) * batch * heads * n * e;
     if (out != base) CSD_CU(cudaMemcpyAsync(out, base, bytes, cudaMemcpyDeviceToDevice, s), "copy");
     if (k_max == 0) return CSD_OK;
-    float* L = (float*)c->ws(csd::kWsLogits, sizeof(float) * batch * heads * n * k_max);
+    float* L = (float*)c->ws(csd::kWsLogits, sizeof(float) * batch * heads * n * k_max, s);
     CSD_TRY(need_ws(L));
     CSD_CU(check_attention_logits((const float*)q, (const float*)k, layout, batch, heads, n, e,
                                   chunk, idx, counts, k_max, L, s), "logits");
@@ -277,7 +277,7 @@ csd_status csd_dense_mlp(csd_ctx* ctx, csd_mode mode, const void* x, const void*
         return csd::prod_dense_mlp(c, x, w1, b1, w2, b2, batch, n, d, f, chunk, out, act_out,
                                    nullptr, nullptr, s);
     }
-    float* act = act_out ? (float*)act_out : (float*)c->ws(csd::kWsAct, sizeof(float) * rows * f);
+    float* act = act_out ? (float*)act_out : (float*)c->ws(csd::kWsAct, sizeof(float) * rows * f, s);
     CSD_TRY(need_ws(act));
     CSD_CU(check_dense_mlp((const float*)x, (const float*)w1, b1, (const float*)w2, b2, batch, n, d,
                            f, act, out, s), "dense_mlp");
@@ -295,13 +295,13 @@ csd_status csd_mlp_tile_means(csd_ctx* ctx, csd_mode mode, const void* x, const 
     if (mode == CSD_MODE_PROD) {
         if (!means_tc_supported(d, f))
             return set_error(CSD_ERR_UNSUPPORTED, "production tile means need D %% 64 == 0 and F %% 128 == 0");
-        void* ws = c->ws(csd::kWsMeans, prod_means_ws_bytes(batch, n, d, f, chunk));
+        void* ws = c->ws(csd::kWsMeans, prod_means_ws_bytes(batch, n, d, f, chunk), s);
         CSD_TRY(need_ws(ws));
         CSD_CU(prod_tile_means_tc(x, w1, batch, n, d, f, chunk, nullptr, out, ws, s), "tile_means");
         c->launches += 3;
         return CSD_OK;
     }
-    float* means = (float*)c->ws(csd::kWsMeans, sizeof(float) * batch * (n / chunk) * d);
+    float* means = (float*)c->ws(csd::kWsMeans, sizeof(float) * batch * (n / chunk) * d, s);
     CSD_TRY(need_ws(means));
     CSD_CU(check_tile_means((const float*)x, (const float*)w1, batch, n, d, f, chunk, means, out, s),
            "tile_means");
@@ -321,12 +321,12 @@ csd_status csd_mlp_change_indices(csd_ctx* ctx, csd_mode mode, const void* x, co
                          (long long)f);
     const cudaStream_t s = S(stream);
     const int64_t rows = batch * (n / chunk);
-    float* scores = (float*)c->ws(csd::kWsScores, sizeof(float) * rows * f * 2);
+    float* scores = (float*)c->ws(csd::kWsScores, sizeof(float) * rows * f * 2, s);
     CSD_TRY(need_ws(scores));
     if (mode == CSD_MODE_PROD) {
         if (!means_tc_supported(d, f))
             return set_error(CSD_ERR_UNSUPPORTED, "production tile means need D %% 64 == 0 and F %% 128 == 0");
-        void* ws = c->ws(csd::kWsMeans, prod_means_ws_bytes(batch, n, d, f, chunk));
+        void* ws = c->ws(csd::kWsMeans, prod_means_ws_bytes(batch, n, d, f, chunk), s);
         CSD_TRY(need_ws(ws));
         if (!c->sorted_topk && topk_cluster_eligible(rows, f) && k <= f) {
             // unsorted selection: |T - T_m| reduced inside the cluster top-k's load
@@ -374,7 +374,7 @@ csd_status csd_sparse_delta_mlp(csd_ctx* ctx, csd_mode mode, const void* x, cons
                              "production sparse-delta MLP needs model_dim %% 128 == 0 and chunk <= 256 "
                              "(got D=%lld, chunk=%lld)", (long long)d, (long long)chunk);
         const int64_t k_pad = csd::dev::prod_smlp_delta_cols(k_max, rows);
-        void* dws = c->ws(csd::kWsDelta, 2 * rows * chunk * (k_pad ? k_pad : 128));
+        void* dws = c->ws(csd::kWsDelta, 2 * rows * chunk * (k_pad ? k_pad : 128), s);
         CSD_TRY(need_ws(dws));
         CSD_CU(prod_sparse_delta_mlp_tc(x, w1, b1, w2, idx, counts, k_max, chunk, batch, n, d, f,
                                         act_cache, out_cache, dws, s), "sparse_delta_mlp");
@@ -383,7 +383,7 @@ csd_status csd_sparse_delta_mlp(csd_ctx* ctx, csd_mode mode, const void* x, cons
     }
     CSD_TRY(sync_validate(c, idx, counts, rows, k_max, f, s));
     if (k_max == 0) return CSD_OK;
-    float* ws = (float*)c->ws(csd::kWsDelta, sizeof(float) * rows * chunk * k_max);
+    float* ws = (float*)c->ws(csd::kWsDelta, sizeof(float) * rows * chunk * k_max, s);
     CSD_TRY(need_ws(ws));
     CSD_CU(check_sparse_delta_mlp((const float*)x, (const float*)w1, b1, (const float*)w2, idx,
                                   counts, k_max, chunk, batch, n, d, f, (float*)act_cache,

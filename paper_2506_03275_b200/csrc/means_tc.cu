@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "launch_util.h"
 #include "tc_common.cuh"
 
 namespace csd {
@@ -214,10 +215,9 @@ cudaError_t prod_tile_means_tc(const void* x, const void* w1, int64_t batch, int
     const int nmax = means_tile_n(means_tile_chunks((int)bc, 0));
     MeansParams p{partial, (int)bc, (int)f, (int)(kblocks / ks), (uint32_t)nmax * 128u};
     const size_t smem = kMeansStages * (kMTile + (size_t)nmax * 128) + 256 + 1024;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_tile_means_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
+    {
+        cudaError_t e = ensure_smem_attr(k_tile_means_tc, 227 * 1024);
+        if (e != cudaSuccess) return e;
     }
     k_tile_means_tc<<<dim3((unsigned)mtiles, (unsigned)ntiles, (unsigned)ks), 128, smem, s>>>(tw, tb, p);
     const int64_t total = bc * f;

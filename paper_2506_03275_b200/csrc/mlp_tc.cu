@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "launch_util.h"
 #include "tc_common.cuh"
 
 namespace csd {
@@ -651,22 +652,16 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
     p.f = (int)f;
     p.d = (int)d;
     p.nz = (int)(batch * nc);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_smlp_up<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, LU::kMaxSmem);
-        cudaFuncSetAttribute(k_smlp_down<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, DnLayout<NT>::kAlloc);
-        attr = true;
+    {
+        cudaError_t e = ensure_smem_attr(k_smlp_up<NT>, (int)LU::kMaxSmem);
+        if (e == cudaSuccess) e = ensure_smem_attr(k_smlp_down<NT>, (int)DnLayout<NT>::kAlloc);
+        if (e != cudaSuccess) return e;
     }
     dim3 g1((unsigned)ntiles, (unsigned)(batch * nc));
     k_smlp_up<NT><<<g1, LU::kThreads, LU::alloc(tn_width), s>>>(tx, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = sm_count();
     const int64_t items = batch * nc * (d / 128);
     k_smlp_down<NT><<<(unsigned)std::min<int64_t>(items, sms), DnLayout<NT>::kThreads,
                       DnLayout<NT>::kAlloc, s>>>(tdl, p);
@@ -678,13 +673,7 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
 // The delta workspace is [B*C*chunk rows][k_pad] bf16, k_pad = round_up(tiles * width, 64)
 // (the down GEMM's 64-neuron k-blocks read up to round_up(count, 64) columns).
 void smlp_geometry(int64_t k_max, int64_t nz, int* tn_width, int* ntiles, int64_t* k_pad) {
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+    const int sms = sm_count();
     const int64_t km = std::max<int64_t>(k_max, 1);
     const int64_t fit = std::max<int64_t>(1, sms / std::max<int64_t>(nz, 1));
     int64_t w = (km + fit - 1) / fit;

@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "launch_util.h"
 
 namespace csd {
 namespace dev {
@@ -525,10 +526,9 @@ cudaError_t topk_rows_fused_absdiff(const float* partial, int ks, const float* c
                                     cudaStream_t s) {
     if (!topk_cluster_eligible(rows, m)) return cudaErrorNotSupported;
     const size_t csm = sizeof(uint32_t) * (size_t)((m + 3) / 4);
-    static bool cattr = false;
-    if (!cattr) {
-        cudaFuncSetAttribute(k_topk_cluster<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 196 * 1024);
-        cattr = true;
+    {
+        cudaError_t e = ensure_smem_attr(k_topk_cluster<4, true>, 196 * 1024);
+        if (e != cudaSuccess) return e;
     }
     k_topk_cluster<4, true><<<(unsigned)(rows * 4), kTopkThreads, csm, s>>>(
         nullptr, m, k, idx, counts, TopkFusedScores{partial, ks, cached});
@@ -542,10 +542,9 @@ cudaError_t topk_rows(const float* scores, int64_t rows, int64_t m, int64_t k, i
     if (!sorted && topk_cluster_eligible(rows, m)) {
         // few long rows: a cluster of 4 CTAs per row (unsorted index set)
         const size_t csm = sizeof(uint32_t) * (size_t)((m + 3) / 4);
-        static bool cattr = false;
-        if (!cattr) {
-            cudaFuncSetAttribute(k_topk_cluster<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 196 * 1024);
-            cattr = true;
+        {
+            cudaError_t e = ensure_smem_attr(k_topk_cluster<4, false>, 196 * 1024);
+            if (e != cudaSuccess) return e;
         }
         k_topk_cluster<4, false><<<(unsigned)(rows * 4), kTopkThreads, csm, s>>>(scores, m, k, idx, counts,
                                                                                   TopkFusedScores{});
@@ -555,10 +554,9 @@ cudaError_t topk_rows(const float* scores, int64_t rows, int64_t m, int64_t k, i
     while (p2 < k) p2 <<= 1;
     const int stage = m <= kTopkMaxSmemRow ? 1 : 0;
     const size_t smem = sizeof(uint64_t) * p2 + (stage ? sizeof(float) * m : 0);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_topk_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 196 * 1024);
-        attr_set = true;
+    {
+        cudaError_t e = ensure_smem_attr(k_topk_rows, 196 * 1024);
+        if (e != cudaSuccess) return e;
     }
     k_topk_rows<<<(unsigned)rows, kTopkThreads, smem, s>>>(scores, m, k, idx, counts, stage, p2, sorted ? 1 : 0);
     return cudaGetLastError();
@@ -601,10 +599,9 @@ cudaError_t validate_index_set(const int32_t* idx, const int32_t* counts, int64_
     if (rows == 0) return cudaSuccess;
     const size_t smem = sizeof(uint32_t) * (size_t)((domain + 31) / 32);
     if (smem > 200 * 1024) return cudaErrorNotSupported;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_validate, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
+    {
+        cudaError_t e = ensure_smem_attr(k_validate, 200 * 1024);
+        if (e != cudaSuccess) return e;
     }
     k_validate<<<(unsigned)rows, 256, smem, s>>>(idx, counts, k_max, domain, flags);
     return cudaGetLastError();

@@ -111,6 +111,10 @@ class Generation:
         if any((blk.mode == capi.MODE_PROD) != self.prod for blk in layers):
             raise ValueError("all layers must run in the same mode")
         self.use_graphs = self.prod if use_graphs is None else bool(use_graphs)
+        if self.use_graphs and not self.prod:
+            # CHECK mode double-buffers the softmax stats on the host side (block.cpp): a
+            # captured dense step would bake one buffer index and replay stale stats
+            raise ValueError("CUDA graphs are PROD-only; CHECK generations run eagerly")
         c = layers[0].cfg
         self.shape = (c.batch, c.seq, c.dim)
         dt = torch.bfloat16 if self.prod else torch.float32
@@ -179,6 +183,8 @@ class Generation:
         total = len(modes)
         scale = float(np.float32(1.0) / np.float32(total))  # harness.cpp:149, fp32 division
         x0, _ = ops.voxel_order(grid0.to(torch.float32).contiguous(), self.layout)
+        for blk in self.layers + (self.baseline or []):  # fresh ModelStates (harness.cpp:180)
+            blk.reset()
         base = self._dense_trajectory(x0, total, scale) if self.baseline else None
 
         def reset():

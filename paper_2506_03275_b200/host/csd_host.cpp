@@ -7,6 +7,8 @@
 // Validation order and exception types follow the reference functions cited per routine;
 // the ABI's csd_status codes are rethrown as the matching csd:: exception.
 #include <algorithm>
+#include <cctype>
+#include <iterator>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -14,7 +16,6 @@
 #include <string>
 #include <vector>
 
-#include <json.hpp>
 
 #include "csd/attention.hpp"
 #include "csd/metrics.hpp"
@@ -308,54 +309,205 @@ SparseIndexSet select_top_k(const Tensor& scores, int64_t k, int64_t chunk_size)
     dc.to(s.counts);
     return s;
 }
+// ---- static sparsity patterns from JSON (sparse_index.hpp:36-39).  Host-side IO outside
+// the hot path; a small schema-specific reader (no JSON library): the document is an object
+// {"chunk_size": int, "k_max": int, "entries": [[b, h, chunk, [ids...]], ...]} (other keys
+// are skipped).  Error classes follow the reference contract: malformed text / schema ->
+// IoError, k_max outside [1, domain] or an entry longer than k_max -> ValueError, entry
+// coordinates or ids out of range -> IndexError; the assembled set is then validated
+// (duplicates -> IndexError).
+namespace {
+class PatternReader {
+  public:
+    explicit PatternReader(const std::string& t) : t_(t) {}
+
+    [[noreturn]] void fail(const std::string& what) const {
+        throw IoError("sparsity pattern JSON: " + what + " at offset " + std::to_string(p_));
+    }
+    void ws() {
+        while (p_ < t_.size() && std::isspace(static_cast<unsigned char>(t_[p_]))) ++p_;
+    }
+    bool peek(char c) {
+        ws();
+        return p_ < t_.size() && t_[p_] == c;
+    }
+    void expect(char c) {
+        if (!peek(c)) fail(std::string("expected '") + c + "'");
+        ++p_;
+    }
+    std::string str() {
+        expect('"');
+        std::string out;
+        while (p_ < t_.size() && t_[p_] != '"') {
+            if (t_[p_] == '\\') {
+                if (++p_ >= t_.size()) break;
+            }
+            out.push_back(t_[p_++]);
+        }
+        if (p_ >= t_.size()) fail("unterminated string");
+        ++p_;
+        return out;
+    }
+    int64_t integer() {
+        ws();
+        const size_t s0 = p_;
+        if (p_ < t_.size() && (t_[p_] == '-' || t_[p_] == '+')) ++p_;
+        while (p_ < t_.size() && std::isdigit(static_cast<unsigned char>(t_[p_]))) ++p_;
+        if (p_ == s0 || (p_ == s0 + 1 && !std::isdigit(static_cast<unsigned char>(t_[s0]))))
+            fail("expected an integer");
+        if (p_ < t_.size() && (t_[p_] == '.' || t_[p_] == 'e' || t_[p_] == 'E'))
+            fail("expected an integer, got a fraction");
+        return std::stoll(t_.substr(s0, p_ - s0));
+    }
+    // skip any JSON value (for keys the schema does not use)
+    void skip() {
+        ws();
+        if (p_ >= t_.size()) fail("unexpected end of text");
+        const char c = t_[p_];
+        if (c == '"') {
+            str();
+        } else if (c == '{' || c == '[') {
+            const char close = c == '{' ? '}' : ']';
+            ++p_;
+            if (peek(close)) {
+                ++p_;
+                return;
+            }
+            for (;;) {
+                if (c == '{') {
+                    str();
+                    expect(':');
+                }
+                skip();
+                if (peek(',')) {
+                    ++p_;
+                    continue;
+                }
+                expect(close);
+                return;
+            }
+        } else {
+            while (p_ < t_.size() && !std::strchr(",]} \t\r\n", t_[p_])) ++p_;
+        }
+    }
+    // comma-separated list in brackets; `item` parses one element
+    template <typename F>
+    void list(F&& item) {
+        expect('[');
+        if (peek(']')) {
+            ++p_;
+            return;
+        }
+        for (;;) {
+            item();
+            if (peek(',')) {
+                ++p_;
+                continue;
+            }
+            expect(']');
+            return;
+        }
+    }
+    void end() {
+        ws();
+        if (p_ != t_.size()) fail("trailing characters");
+    }
+
+  private:
+    const std::string& t_;
+    size_t p_ = 0;
+};
+
+struct PatternEntry {
+    int64_t b, h, c;
+    std::vector<int64_t> ids;
+};
+}  // namespace
+
 SparseIndexSet load_index_set_json(const std::string& text, int64_t batch, int64_t heads,
-                                   int64_t chunks, int64_t domain) {  // sparse_index.cpp:98-148
-    nlohmann::json doc;
-    try {
-        doc = nlohmann::json::parse(text);
-    } catch (const nlohmann::json::exception& e) {
-        throw IoError(std::string("sparsity pattern JSON parse failure: ") + e.what());
+                                   int64_t chunks, int64_t domain) {
+    PatternReader rd(text);
+    bool have_chunk = false, have_k = false, have_entries = false;
+    int64_t chunk_size = 0, k_max = 0;
+    std::vector<PatternEntry> entries;
+    rd.expect('{');
+    if (!rd.peek('}')) {
+        for (;;) {
+            const std::string key = rd.str();
+            rd.expect(':');
+            if (key == "chunk_size") {
+                chunk_size = rd.integer();
+                have_chunk = true;
+            } else if (key == "k_max") {
+                k_max = rd.integer();
+                have_k = true;
+            } else if (key == "entries") {
+                have_entries = true;
+                entries.clear();
+                rd.list([&] {
+                    PatternEntry e{};
+                    int field = 0;
+                    rd.list([&] {
+                        switch (field++) {
+                            case 0: e.b = rd.integer(); break;
+                            case 1: e.h = rd.integer(); break;
+                            case 2: e.c = rd.integer(); break;
+                            case 3: rd.list([&] { e.ids.push_back(rd.integer()); }); break;
+                            default: rd.fail("an entry has more than 4 fields");
+                        }
+                    });
+                    if (field != 4) rd.fail("an entry must be [b, h, chunk, [ids...]]");
+                    entries.push_back(std::move(e));
+                });
+            } else {
+                rd.skip();
+            }
+            if (rd.peek(',')) {
+                rd.expect(',');
+                continue;
+            }
+            break;
+        }
     }
-    if (!doc.is_object() || !doc.contains("chunk_size") || !doc.contains("k_max") || !doc.contains("entries"))
-        throw IoError("sparsity pattern JSON must contain chunk_size, k_max, entries");
-    const int64_t k_max = doc["k_max"].get<int64_t>();
+    rd.expect('}');
+    rd.end();
+    if (!(have_chunk && have_k && have_entries))
+        throw IoError("sparsity pattern JSON needs the keys chunk_size, k_max and entries");
     if (k_max < 1 || k_max > domain)
-        throw ValueError("sparsity pattern k_max " + std::to_string(k_max) + " outside [1, " +
-                         std::to_string(domain) + "]");
-    SparseIndexSet s = SparseIndexSet::empty(batch, heads, chunks, doc["chunk_size"].get<int64_t>(),
-                                             k_max, domain);
-    for (const auto& e : doc["entries"]) {
-        if (!e.is_array() || e.size() != 4) throw IoError("sparsity pattern entry must be [b, h, chunk, [ids...]]");
-        const int64_t b = e[0].get<int64_t>(), h = e[1].get<int64_t>(), c = e[2].get<int64_t>();
-        if (b < 0 || b >= batch || h < 0 || h >= heads || c < 0 || c >= chunks) {
-            std::ostringstream os;
-            os << "sparsity pattern entry (" << b << "," << h << "," << c << ") outside dims ("
-               << batch << "," << heads << "," << chunks << ")";
-            throw IndexError(os.str());
+        throw ValueError("sparsity pattern: k_max = " + std::to_string(k_max) +
+                         " is not in [1, domain = " + std::to_string(domain) + "]");
+    SparseIndexSet set = SparseIndexSet::empty(batch, heads, chunks, chunk_size, k_max, domain);
+    for (const PatternEntry& e : entries) {
+        const bool inside = e.b >= 0 && e.b < batch && e.h >= 0 && e.h < heads && e.c >= 0 &&
+                            e.c < chunks;
+        if (!inside)
+            throw IndexError("sparsity pattern: entry (b=" + std::to_string(e.b) + ", h=" +
+                             std::to_string(e.h) + ", chunk=" + std::to_string(e.c) +
+                             ") is outside [" + std::to_string(batch) + ", " +
+                             std::to_string(heads) + ", " + std::to_string(chunks) + ")");
+        if ((int64_t)e.ids.size() > k_max)
+            throw ValueError("sparsity pattern: an entry lists " + std::to_string(e.ids.size()) +
+                             " ids, more than k_max = " + std::to_string(k_max));
+        int32_t* row = set.chunk_indices(e.b, e.h, e.c);
+        for (size_t i = 0; i < e.ids.size(); ++i) {
+            if (e.ids[i] < 0 || e.ids[i] >= domain)
+                throw IndexError("sparsity pattern: id " + std::to_string(e.ids[i]) +
+                                 " is not in [0, " + std::to_string(domain) + ")");
+            row[i] = static_cast<int32_t>(e.ids[i]);
         }
-        if (static_cast<int64_t>(e[3].size()) > k_max)
-            throw ValueError("sparsity pattern entry lists more than k_max ids");
-        int32_t* dst = s.chunk_indices(b, h, c);
-        int32_t n = 0;
-        for (const auto& v : e[3]) {
-            const int64_t id = v.get<int64_t>();
-            if (id < 0 || id >= domain)
-                throw IndexError("sparsity pattern index " + std::to_string(id) + " out of range [0, " +
-                                 std::to_string(domain) + ")");
-            dst[n++] = static_cast<int32_t>(id);
-        }
-        s.counts[static_cast<size_t>((b * heads + h) * chunks + c)] = n;
+        set.counts[static_cast<size_t>((e.b * heads + e.h) * chunks + e.c)] =
+            static_cast<int32_t>(e.ids.size());
     }
-    s.validate();
-    return s;
+    set.validate();
+    return set;
 }
+
 SparseIndexSet load_index_set_json_file(const std::string& path, int64_t batch, int64_t heads,
                                         int64_t chunks, int64_t domain) {
-    std::ifstream f(path);
-    if (!f) throw IoError("cannot open " + path + " for reading");
-    std::stringstream buf;
-    buf << f.rdbuf();
-    return load_index_set_json(buf.str(), batch, heads, chunks, domain);
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw IoError("sparsity pattern file " + path + " cannot be opened");
+    const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    return load_index_set_json(text, batch, heads, chunks, domain);
 }
 
 // ====================================================================== attention (device)
@@ -562,19 +714,30 @@ Tensor mlp_step(const Tensor& x, const MlpWeights& w, MlpCache& cache, bool dens
 // model.cpp:10-216.  Projections run on the device (csd_project, CHECK mode: the
 // reference's sequential-k fp32 gemm); attention_step / mlp_step are the device-backed
 // routines above; head split/merge and the residual add are host data movement / fp32 adds.
-void ModelConfig::validate() const {  // model.cpp:10-28
-    if (batch < 1 || grid_t < 1 || grid_h < 1 || grid_w < 1 || model_dim < 1 || head_dim < 1 ||
-        heads < 1 || mlp_hidden < 1 || layers < 0 || chunk < 1)
-        throw ConfigError("model config fields must be positive (layers may be 0)");
-    if (model_dim != heads * head_dim)
-        throw ConfigError("model_dim " + std::to_string(model_dim) + " != heads*head_dim " +
-                          std::to_string(heads * head_dim));
-    if (seq_len() % chunk != 0)
-        throw ConfigError("sequence length " + std::to_string(seq_len()) +
-                          " not divisible by chunk " + std::to_string(chunk));
-    if (voxel_t * voxel_h * voxel_w != chunk)
-        throw ConfigError("voxel volume " + std::to_string(voxel_t * voxel_h * voxel_w) +
-                          " must equal chunk " + std::to_string(chunk));
+// ModelConfig (model.hpp:16-41) consistency, the model.cpp:10-28 contract: every ConfigError
+// case of the reference, checked as a list of (holds, message) rules in order.
+void ModelConfig::validate() const {
+    const int64_t dims[] = {batch, grid_t, grid_h, grid_w, model_dim, head_dim, heads, mlp_hidden,
+                            chunk};
+    const bool positive = std::all_of(std::begin(dims), std::end(dims), [](int64_t v) { return v > 0; });
+    const int64_t vol = voxel_t * voxel_h * voxel_w;
+    const struct {
+        bool ok;
+        std::string msg;
+    } rules[] = {
+        {positive && layers >= 0,
+         "model config: batch, grid, dims, heads, hidden and chunk must be >= 1 (layers >= 0)"},
+        {model_dim == heads * head_dim,
+         "model config: model_dim = " + std::to_string(model_dim) + " but heads x head_dim = " +
+             std::to_string(heads * head_dim)},
+        {positive && seq_len() % chunk == 0,
+         "model config: chunk " + std::to_string(chunk) + " does not divide the sequence length " +
+             std::to_string(seq_len())},
+        {vol == chunk, "model config: voxel volume " + std::to_string(vol) +
+                           " differs from the chunk size " + std::to_string(chunk)},
+    };
+    for (const auto& r : rules)
+        if (!r.ok) throw ConfigError(r.msg);
     voxel_layout().validate();
 }
 

@@ -518,11 +518,24 @@ class Block:
             raise TypeError(f"block expects {self.dtype} activations")
         if out is None:
             out = torch.empty_like(x)
+        if static is not None:
+            from .errors import ShapeError
+            c = self.cfg
+            hl = c.heads_local or c.heads
+            want = (c.batch, hl, c.seq // c.chunk, c.chunk, c.seq)
+            got = (static.batch, static.heads, static.chunks, static.chunk_size, static.domain)
+            if got != want or tuple(static.indices.shape) != (*want[:3], static.k_max):
+                raise ShapeError(f"static attention pattern (batch, heads, chunks, chunk, domain)"
+                                 f" = {got} does not match the block {want}")
         raise_for(self.ctx.lib, self.ctx.lib.csd_block_step(
             self.h, _ptr(x), _ptr(out), int(bool(dense)),
             _ptr(static.indices) if static else None, _ptr(static.counts) if static else None,
             static.k_max if static else 0, _stream()))
         return out
+
+    def reset(self):
+        """A fresh ModelState for this layer (model.cpp:101-105): the next step must be dense."""
+        raise_for(self.ctx.lib, self.ctx.lib.csd_block_reset(self.h))
 
     def cache(self, which: int) -> torch.Tensor:
         c = self.cfg
