@@ -29,6 +29,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -75,9 +76,13 @@ struct AttnLayout {
     static constexpr uint32_t kKV = kHalves * kStrip;  // one K or V block
     static constexpr uint32_t kCsBytes = 2 * 4 * NT * 128 * 4;  // colsum partials [2][NT][4][128]
     static constexpr uint32_t kXchBytes = 2 * 128 * 2 * 4;       // row-half exchange [2][128][2]
-    // 4 control warps (producers, MMA, I/O) + 8 softmax warps: two per TMEM lane quadrant,
-    // each owning 64 of a row's 128 key columns
-    static constexpr uint32_t kThreads = 128 + 256;
+    // warpgroup 0: warp 0 (Q / dense K-V TMA, staged-base I/O), warp 1 (MMA), warps 2-3
+    // (K/V row copies); warpgroups 1-2: 8 softmax warps, two per TMEM lane quadrant, each
+    // owning 64 of a row's 128 key columns; warpgroup 3: four more K/V copy warps.
+    static constexpr uint32_t kThreads = 128 + 256 + 128;
+    // sparse K/V rows are staged by cp.async from 6 copy warps (warps 2, 3, 12-15): 16 threads
+    // per 256-byte row, 16-byte pieces written straight into the 128B-swizzled strips
+    static constexpr int kCopyThreads = 192;
     static constexpr uint32_t kTmemCols = (NT * 128 + NT * E) <= 256 ? 256 : 512;
     static constexpr uint32_t kMaxSmem = 227 * 1024;
 };
@@ -102,6 +107,9 @@ struct AttnParams {
     int layout;
     int heads, n, chunk, chunks, items;
     int cs_chunk, cs_chunks;  // colsum chunking when it differs from the item rows (else 0)
+    const __nv_bfloat16* kp;  // raw K / V (the cp.async row gather)
+    const __nv_bfloat16* vp;
+    int cp_async;             // sparse K/V staging: 1 = cp.async copy warps, 0 = TMA gather4
     uint64_t* trace;          // debug timeline (null: off)
     uint64_t* span;           // debug per-CTA [start, end] globaltimer (null: off)
     float qk_scale_log2;  // log2(e) / sqrt(E)
@@ -154,10 +162,13 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         // the host sizes the request without alignment slack (the 227 KB budget is tight)
         if ((raw_u32 & 1023u) != 0) __trap();
         mbar_init(bar_q, 1);
+        // cp.async staging: one cp.async.mbarrier arrival per copy thread per block;
+        // TMA (tiles / gather4): one expect_tx arrival
+        const uint32_t fill = (!dense && p.cp_async) ? (uint32_t)L::kCopyThreads : 1u;
         for (int i = 0; i < 2; ++i) {
-            mbar_init(bar_kf + i, 1);
+            mbar_init(bar_kf + i, fill);
             mbar_init(bar_ke + i, 1);
-            mbar_init(bar_vf + i, 1);
+            mbar_init(bar_vf + i, fill);
             mbar_init(bar_ve + i, 1);
         }
         for (int t = 0; t < NT; ++t) {
@@ -176,6 +187,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) ATTN_TRACE(1);
+    const bool cpa = !dense && p.cp_async;
     // next live (count > 0) item of this CTA at or after `from`
     auto next_live = [&](int from, int& cnt_out) -> int {
         int x = from;
@@ -199,7 +211,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 tma_load_2d(&tm_b, bar_bf, sx + hf * p.x_strip + bx * 8192, cl2 + hf * 64,
                             rb2 + (it % p.chunks) * p.chunk + bx * 64);
     };
-    // staged-base I/O thread (warp 1 lane 1; lane 0 issues the MMAs): per live item, base
+    // staged-base I/O thread (warp 0 lane 31): per live item, base
     // tile in, then -- once every softmax warp has combined its rows in place -- the out tile
     // out by TMA store, then the next item's base tile in
     auto io_thread = [&]() {
@@ -228,15 +240,13 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         bulk_wait0();  // the last out tile has landed before the CTA exits
     };
     // ---------------------------------------------------------------- producers
-    // Warps 0/2/3 spread the sparse blocks' tile::gather4s (one warp's TMA issue is
-    // serialised); dense blocks are plain TMA tiles from warp 0.
-    auto producer = [&]() {
-        const int pw = warp == 0 ? 0 : warp - 1;
-        const bool mine = (lane % 3) == pw;
-        if (warp == 0 && lane == 0) {
-            tma_prefetch_desc(&tm_q);
-            tma_prefetch_desc(dense ? &tm_k : &tm_kg);
-            tma_prefetch_desc(dense ? &tm_v : &tm_vg);
+    // Every loader walks the same live-item / key-block sequence (counters li, gb).
+    // Q tiles (all modes) and the dense K/V tiles: warp 0 lane 0, plain TMA.
+    auto q_loader = [&]() {
+        tma_prefetch_desc(&tm_q);
+        if (dense) {
+            tma_prefetch_desc(&tm_k);
+            tma_prefetch_desc(&tm_v);
         }
         uint32_t gb = 0, li = 0;
         for (int item = blockIdx.x; item < items; item += gridDim.x) {
@@ -247,71 +257,151 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             const int row_base = p.layout == CSD_LAYOUT_BHNE ? bh * p.n : b * p.n;
             const int col0 = p.layout == CSD_LAYOUT_BHNE ? 0 : h * E;
             const int nblk = (cnt + 127) / 128;
-            if (warp == 0 && lane == 0) {
-                if (li > 0) mbar_wait(bar_qe, (li - 1) & 1);  // previous item's S MMAs done
-                ATTN_TRACE(2 + li);
-                mbar_arrive_expect_tx(bar_q, (uint32_t)(L::kHalves * (p.q_rows[0] + (NT > 1 ? p.q_rows[1] : 0))) * 128u);
-                for (int t = 0; t < NT; ++t)
+            if (li > 0) mbar_wait(bar_qe, (li - 1) & 1);  // previous item's S MMAs done
+            ATTN_TRACE(2 + li);
+            mbar_arrive_expect_tx(bar_q, (uint32_t)(L::kHalves * (p.q_rows[0] + (NT > 1 ? p.q_rows[1] : 0))) * 128u);
+            for (int t = 0; t < NT; ++t)
+                for (int hf = 0; hf < L::kHalves; ++hf)
+                    for (int bx = 0; bx < p.q_rows[t] / 64; ++bx)  // 64-row boxes
+                        tma_load_2d(&tm_q, bar_q, sq + p.q_off[t] + hf * p.q_strip[t] + bx * 8192,
+                                    col0 + hf * 64, row_base + c * p.chunk + t * 128 + bx * 64);
+            if (dense) {
+                for (int j = 0; j < nblk; ++j, ++gb) {
+                    const int s = gb & 1;
+                    if (gb >= 2) mbar_wait(bar_ke + s, ((gb >> 1) - 1) & 1);
+                    ATTN_TRACE(16 + gb);
+                    mbar_arrive_expect_tx(bar_kf + s, L::kKV);
                     for (int hf = 0; hf < L::kHalves; ++hf)
-                        for (int bx = 0; bx < p.q_rows[t] / 64; ++bx)  // 64-row boxes
-                            tma_load_2d(&tm_q, bar_q, sq + p.q_off[t] + hf * p.q_strip[t] + bx * 8192,
-                                        col0 + hf * 64, row_base + c * p.chunk + t * 128 + bx * 64);
-            }
-            const int32_t* ids = dense ? nullptr : p.idx + (int64_t)item * p.k_max;
-            for (int j = 0; j < nblk; ++j, ++gb) {
-                const int s = gb & 1;
-                int32_t rows[4] = {0, 0, 0, 0};
-                if (!dense) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        int r = j * 128 + lane * 4 + i;
-                        r = r < cnt ? r : cnt - 1;  // pad with a valid row (masked in softmax)
-                        rows[i] = row_base + __ldg(ids + r);
-                    }
-                }
-                if (gb >= 2) mbar_wait(bar_ke + s, ((gb >> 1) - 1) & 1);
-                // K_j -> ring slot s
-                if (warp == 0 && lane == 0) ATTN_TRACE(16 + gb);
-                if (warp == 0 && lane == 0) mbar_arrive_expect_tx(bar_kf + s, L::kKV);
-                uint8_t* kdst = sk + s * L::kKV;
-                if (dense) {
-                    if (warp == 0 && lane == 0)
-                        for (int hf = 0; hf < L::kHalves; ++hf)
-                            tma_load_2d(&tm_k, bar_kf + s, kdst + hf * L::kStrip, col0 + hf * 64,
-                                        row_base + j * 128);
-                } else if (mine) {
+                        tma_load_2d(&tm_k, bar_kf + s, sk + s * L::kKV + hf * L::kStrip, col0 + hf * 64,
+                                    row_base + j * 128);
+                    if (gb >= 2) mbar_wait(bar_ve + s, ((gb >> 1) - 1) & 1);
+                    mbar_arrive_expect_tx(bar_vf + s, L::kKV);
                     for (int hf = 0; hf < L::kHalves; ++hf)
-                        tma_gather4(&tm_kg, bar_kf + s, kdst + hf * L::kStrip + lane * 512,
-                                    col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
+                        tma_load_2d(&tm_v, bar_vf + s, sv + s * L::kKV + hf * L::kStrip, col0 + hf * 64,
+                                    row_base + j * 128);
+                    ATTN_TRACE(48 + gb);
                 }
-                // V_j -> ring slot s
-                if (gb >= 2) mbar_wait(bar_ve + s, ((gb >> 1) - 1) & 1);
-                if (warp == 0 && lane == 0) mbar_arrive_expect_tx(bar_vf + s, L::kKV);
-                uint8_t* vdst = sv + s * L::kKV;
-                if (dense) {
-                    if (warp == 0 && lane == 0)
-                        for (int hf = 0; hf < L::kHalves; ++hf)
-                            tma_load_2d(&tm_v, bar_vf + s, vdst + hf * L::kStrip, col0 + hf * 64,
-                                        row_base + j * 128);
-                } else if (mine) {
-                    for (int hf = 0; hf < L::kHalves; ++hf)
-                        tma_gather4(&tm_vg, bar_vf + s, vdst + hf * L::kStrip + lane * 512,
-                                    col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
-                }
-                if (warp == 0 && lane == 0) ATTN_TRACE(48 + gb);
             }
             ++li;
         }
     };
-    if (warp == 0 || warp == 2 || warp == 3) {
-        // warp 3 lane 31 issues no gathers (lane % 3 != 2): it runs the staged-base I/O
-        if (warp == 3 && lane == 31) {
-            if (p.stage_base) io_thread();
-        } else {
-            producer();
+    // Sparse K/V rows by TMA tile::gather4 (4 rows per instruction, one instruction per
+    // 64-column strip), spread over three warps (lane % 3 == pw).
+    auto gather4_loader = [&](int pw) {
+        const bool mine = (lane % 3) == pw;
+        if (pw == 0 && lane == 0) {
+            tma_prefetch_desc(&tm_kg);
+            tma_prefetch_desc(&tm_vg);
         }
-    } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
+        uint32_t gb = 0;
+        for (int item = blockIdx.x; item < items; item += gridDim.x) {
+            const int cnt = p.counts[item];
+            if (cnt == 0) continue;
+            const int bh = item / p.chunks;
+            const int b = bh / p.heads, h = bh % p.heads;
+            const int row_base = p.layout == CSD_LAYOUT_BHNE ? bh * p.n : b * p.n;
+            const int col0 = p.layout == CSD_LAYOUT_BHNE ? 0 : h * E;
+            const int nblk = (cnt + 127) / 128;
+            const int32_t* ids = p.idx + (int64_t)item * p.k_max;
+            for (int j = 0; j < nblk; ++j, ++gb) {
+                const int s = gb & 1;
+                int32_t rows[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    int r = j * 128 + lane * 4 + i;
+                    r = r < cnt ? r : cnt - 1;  // pad with a valid row (masked in softmax)
+                    rows[i] = row_base + __ldg(ids + r);
+                }
+                if (gb >= 2) mbar_wait(bar_ke + s, ((gb >> 1) - 1) & 1);
+                if (pw == 0 && lane == 0) mbar_arrive_expect_tx(bar_kf + s, L::kKV);
+                if (mine)
+                    for (int hf = 0; hf < L::kHalves; ++hf)
+                        tma_gather4(&tm_kg, bar_kf + s, sk + s * L::kKV + hf * L::kStrip + lane * 512,
+                                    col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
+                if (gb >= 2) mbar_wait(bar_ve + s, ((gb >> 1) - 1) & 1);
+                if (pw == 0 && lane == 0) mbar_arrive_expect_tx(bar_vf + s, L::kKV);
+                if (mine)
+                    for (int hf = 0; hf < L::kHalves; ++hf)
+                        tma_gather4(&tm_vg, bar_vf + s, sv + s * L::kKV + hf * L::kStrip + lane * 512,
+                                    col0 + hf * 64, rows[0], rows[1], rows[2], rows[3]);
+            }
+        }
+    };
+    // Sparse K/V rows by cp.async (LSU path, ~2.5x gather4's per-SM rate): copy thread ct
+    // owns the fixed 16-byte pieces ct + kCopyThreads * i of every block (16 pieces per
+    // 256-byte row, consecutive threads on one row), written straight into the 128B-swizzled
+    // strips; rows past the chunk's count are zero-filled (src-size 0: no global read), so
+    // the dead key columns of the last block hold finite zeros.  One
+    // cp.async.mbarrier.arrive.noinc per thread per K (V) block completes the fill barrier.
+    auto copy_loader = [&](int ct) {
+        // kCopyThreads = 12 x 16: thread ct always copies 16-byte column piece c16 = ct % 16
+        // of rows r0 + 12 i (r0 = ct / 16), i.e. the same smem column slot in every block
+        static_assert(L::kCopyThreads % (E / 8) == 0, "copy threads per row");
+        constexpr int kRowStep = L::kCopyThreads / (E / 8);
+        constexpr int kRows = (128 + kRowStep - 1) / kRowStep;
+        const int c16 = ct % (E / 8), r0 = ct / (E / 8);
+        const uint32_t cbase = (uint32_t)(c16 >> 3) * L::kStrip;
+        const int64_t rs = p.layout == CSD_LAYOUT_BHNE ? E : (int64_t)p.heads * E;  // row stride
+        const uint32_t sK = smem_u32(sk), sV = smem_u32(sv);
+        uint32_t gb = 0;
+        for (int item = blockIdx.x; item < items; item += gridDim.x) {
+            const int cnt = p.counts[item];
+            if (cnt == 0) continue;
+            const int bh = item / p.chunks;
+            const int b = bh / p.heads, h = bh % p.heads;
+            const int64_t o0 = tok_elem_off(p.layout, b, h, 0, p.heads, p.n, E) + c16 * 8;
+            const __nv_bfloat16* kb = p.kp + o0;
+            const __nv_bfloat16* vb = p.vp + o0;
+            const int nblk = (cnt + 127) / 128;
+            const int32_t* ids = p.idx + (int64_t)item * p.k_max;
+            for (int j = 0; j < nblk; ++j, ++gb) {
+                const int s = gb & 1;
+                int32_t id[kRows];
+#pragma unroll
+                for (int i = 0; i < kRows; ++i) {
+                    const int r = j * 128 + r0 + kRowStep * i;
+                    id[i] = (r0 + kRowStep * i < 128 && r < cnt) ? __ldg(ids + r) : -1;
+                }
+                if (gb >= 2) mbar_wait(bar_ke + s, ((gb >> 1) - 1) & 1);
+#pragma unroll
+                for (int i = 0; i < kRows; ++i) {
+                    const uint32_t row = (uint32_t)(r0 + kRowStep * i);
+                    if (row < 128u)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                                         sK + s * L::kKV + cbase + sw128_offset(row, (uint32_t)(c16 & 7))),
+                                     "l"(kb + (id[i] >= 0 ? (int64_t)id[i] * rs : 0)), "r"(id[i] >= 0 ? 16u : 0u)
+                                     : "memory");
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar_kf + s)) : "memory");
+                if (gb >= 2) mbar_wait(bar_ve + s, ((gb >> 1) - 1) & 1);
+#pragma unroll
+                for (int i = 0; i < kRows; ++i) {
+                    const uint32_t row = (uint32_t)(r0 + kRowStep * i);
+                    if (row < 128u)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                                         sV + s * L::kKV + cbase + sw128_offset(row, (uint32_t)(c16 & 7))),
+                                     "l"(vb + (id[i] >= 0 ? (int64_t)id[i] * rs : 0)), "r"(id[i] >= 0 ? 16u : 0u)
+                                     : "memory");
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar_vf + s)) : "memory");
+            }
+        }
+    };
+    // Registers go to the softmax warpgroups (1, 2): 4 x 128 x 128 at launch = 2 x 128 x 72 +
+    // 2 x 128 x 184.  Each role branch starts with its warpgroup's setmaxnreg so the
+    // register budget of the code below it is known to ptxas.
+    if (warp < 4 || warp >= 12) {
+    regs_dec<72>();
+    if (warp == 0) {
+        if (lane == 0) q_loader();
+        else if (lane == 31 && p.stage_base) io_thread();
+    } else if (warp == 2 || warp == 3 || warp >= 12) {
+        if (!dense) {
+            if (p.cp_async) copy_loader(warp < 4 ? (warp - 2) * 32 + lane : 64 + (warp - 12) * 32 + lane);
+            else if (warp <= 12) gather4_loader(warp == 12 ? 2 : warp - 2);
+        }
+    } else {
+        // ------------------------------------------------------------ MMA issuer (warp 1)
         // The whole warp walks the schedule so the descriptors are warp-uniform (uniform
         // registers, no per-MMA broadcast); lane 0 (elect.sync's leader) issues every MMA
         // and commit, so the commits track that lane's MMAs.
@@ -363,6 +453,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 mbar_wait(bar_q, li & 1);
                 ATTN_TRACE(8 + li);
                 mbar_wait(bar_kf + (gb & 1), (gb >> 1) & 1);
+                if (cpa) fence_proxy_async_smem();  // cp.async (generic proxy) -> tcgen05 reads
                 tc_fence_after();
                 ATTN_TRACE(80 + gb);
                 for (int t = 0; t < NT; ++t) issue_s(t, gb);
@@ -377,6 +468,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                         mbar_wait(bar_p + t, g & 1);
                         if (t == 0) {
                             mbar_wait(bar_vf + (g & 1), (g >> 1) & 1);
+                            if (cpa) fence_proxy_async_smem();
                             ATTN_TRACE(832 + (g & 63));
                         }
                         tc_fence_after();
@@ -386,6 +478,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                         if (more) {
                             if (t == 0) {
                                 mbar_wait(bar_kf + ((g + 1) & 1), ((g + 1) >> 1) & 1);
+                                if (cpa) fence_proxy_async_smem();
                                 tc_fence_after();
                                 ATTN_TRACE(80 + g + 1);
                                 ATTN_TRACE(768 + ((g + 1) & 63));
@@ -404,7 +497,9 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 ++li;
             }
         }
+    }
     } else {
+        regs_inc<184>();
         // ------------------------------------------------------------ softmax / epilogue
         // 8 warps: warp 4 + 4 hf + quad owns TMEM lane quadrant `quad` (rows quad * 32 + lane
         // of every M-tile) and key columns [64 hf, 64 hf + 64) of each S block.  The two
@@ -695,7 +790,7 @@ k_attn_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                     }
                 }
                 if (lane == 0 && sw == 0) ATTN_TRACE(232 + li);
-                // hand X to the I/O thread (warp 1 lane 1): it stores the out tile by TMA and
+                // hand X to the I/O thread (warp 0 lane 31): it stores the out tile by TMA and
                 // refills X with the next live item's base tile; the softmax warps go on
                 fence_proxy_async_smem();  // this thread's in-place writes -> async proxy
                 __syncwarp();
@@ -838,6 +933,17 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
     p.n = (int)a.n;
     p.chunk = (int)a.chunk;
     p.chunks = (int)(a.n / a.chunk);
+    p.kp = static_cast<const __nv_bfloat16*>(a.k);
+    p.vp = static_cast<const __nv_bfloat16*>(a.v);
+    {
+        // sparse K/V staging path: cp.async copy warps (default) or TMA gather4
+        // (CSD_ATTN_GATHER=g4, for comparison)
+        static const int cp = [] {
+            const char* e = std::getenv("CSD_ATTN_GATHER");
+            return (e && std::string(e) == "g4") ? 0 : 1;
+        }();
+        p.cp_async = cp;
+    }
     p.trace = h_attn_trace;
     p.span = h_attn_span;
     p.cs_chunk = (a.colsum != nullptr && a.cs_chunk > 0 && a.cs_chunk != a.chunk) ? (int)a.cs_chunk : 0;
