@@ -400,7 +400,7 @@ def profiled_traffic(kernel_substr):
         return None
 
 
-def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps, dense_ms=None):
+def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps, dense_ms=None, flush_l2=True):
     """Sparse (k = attn_k) vs dense (all N keys, same kernel family) attention on the FLUX
     shape, inputs resident in HBM, L2 flushed between repetitions."""
     h, e, c = cfg["heads"], cfg["head_dim"], cfg["chunk"]
@@ -432,7 +432,8 @@ def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps, dense_ms=None):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(reps + 3)]
         for i, (a, b) in enumerate(evs):
-            flush.fill_(float(i))  # evict L2 (256 MB write) between repetitions
+            if flush_l2:
+                flush.fill_(float(i))  # evict L2 (256 MB write) between repetitions
             a.record(stream)
             g.replay()
             b.record(stream)
@@ -455,7 +456,8 @@ def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps, dense_ms=None):
             "dense": {"ms": round(t_dense, 5), "flops": dense_flops,
                       "tflops": round(dense_flops / (t_dense * 1e-3) / 1e12, 2)},
             "speedup_vs_dense": round(t_dense / t_sparse, 3),
-            "k": attn_k, "n": n, "reps": reps, "l2_flush": "256 MB write between reps"}
+            "k": attn_k, "n": n, "reps": reps,
+            "l2_flush": "256 MB write between reps" if flush_l2 else "none (L2 warm)"}
 
 
 def mlp_kernel_bench(ops, torch, cfg, n, mlp_k, reps):

@@ -101,6 +101,10 @@ struct AttnTcArgs {
 // Returns cudaErrorNotSupported for shapes outside the envelope.
 cudaError_t attn_tc(const AttnTcArgs& a, cudaStream_t s);
 bool attn_tc_supported(int64_t e, int64_t chunk);
+// attn_pp.cu: ping-pong-tile kernel for items of 129..256 rows without column sums
+// (CSD_ATTN_KERNEL=tc forces k_attn_tc); attn_tc() dispatches to it.
+bool attn_pp_supported(const AttnTcArgs& a);
+cudaError_t attn_pp(const AttnTcArgs& a, cudaStream_t s);
 
 cudaError_t prod_cast_f32_bf16(const float* in, void* out, int64_t n, cudaStream_t s);
 cudaError_t prod_cast_bf16_f32(const void* in, float* out, int64_t n, cudaStream_t s);

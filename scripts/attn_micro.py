@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--sparsity", type=float, default=0.93)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between reps")
     args = ap.parse_args()
     cfg = dict(bench.FLUX)
     n = cfg["grid"][1] * cfg["grid"][2]
@@ -46,7 +47,7 @@ def main():
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
         return
-    res = bench.attention_kernel_bench(ops, torch, cfg, n, ak, args.reps)
+    res = bench.attention_kernel_bench(ops, torch, cfg, n, ak, args.reps, flush_l2=not args.no_flush)
     print(json.dumps(res))
 
 
