@@ -237,10 +237,18 @@ csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int den
     const int64_t mk = c.mlp_k > 0 ? c.mlp_k : Fl;
     CSD_TRY(attn_core(blk, x_in, dense, static_idx, static_counts, static_k_max, stream));
     if (md == CSD_MODE_PROD) {
-        // x1 = x + O Wo: the residual rides in the GEMM (C = x, beta = 1, fp32 accumulate)
-        CSD_CU(cudaMemcpyAsync(blk->x_mid, x_in, 2 * B * N * D, cudaMemcpyDeviceToDevice, s), "copy");
-        CSD_TRY(csd::gemm_bf16(blk->ctx, blk->attn, blk->wo, false, blk->x_mid, false, B * N, D, Dl,
-                               1.0f, s));
+        // x1 = x + O Wo: the residual rides in the GEMM epilogue (gemm_tc.cu); the library
+        // fallback adds it as C = x, beta = 1 over a copy
+        if (csd::dev::gemm_tc_enabled() && csd::dev::gemm_tc_proj_supported(B * N, Dl, D)) {
+            const void* w[3] = {blk->wo, blk->wo, blk->wo};
+            void* o[3] = {blk->x_mid, blk->x_mid, blk->x_mid};
+            CSD_CU(csd::dev::gemm_tc_proj(blk->attn, w, o, 1, B * N, Dl, D, x_in, s), "gemm_tc_wo");
+            blk->ctx->launches += 1;
+        } else {
+            CSD_CU(cudaMemcpyAsync(blk->x_mid, x_in, 2 * B * N * D, cudaMemcpyDeviceToDevice, s), "copy");
+            CSD_TRY(csd::gemm_bf16(blk->ctx, blk->attn, blk->wo, false, blk->x_mid, false, B * N, D,
+                                   Dl, 1.0f, s));
+        }
         // ---- MLP branch; x2 = x1 + M is fused into the last MLP kernel's epilogue
         if (dense) {
             CSD_TRY(csd::prod_dense_mlp(blk->ctx, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B,
@@ -292,9 +300,18 @@ static csd_status attn_core(csd_block* blk, const void* x_in, int dense, const i
     const int64_t B = c.batch, N = c.seq, D = c.dim, E = c.head_dim, Hl = c.heads_local;
     const int64_t Dl = Hl * E, C = N / c.chunk;
     const int64_t ak = blk->a_kmax;
-    CSD_TRY(csd_project(ctx, md, x_in, blk->wq, B, N, D, Dl, blk->q, stream));
-    CSD_TRY(csd_project(ctx, md, x_in, blk->wk, B, N, D, Dl, blk->k, stream));
-    CSD_TRY(csd_project(ctx, md, x_in, blk->wv, B, N, D, Dl, blk->v, stream));
+    if (md == CSD_MODE_PROD && csd::dev::gemm_tc_enabled() &&
+        csd::dev::gemm_tc_proj_supported(B * N, D, Dl)) {
+        // one tcgen05 launch for the three projections (gemm_tc.cu), bf16 [B, N, H, E] out
+        const void* w[3] = {blk->wq, blk->wk, blk->wv};
+        void* o[3] = {blk->q, blk->k, blk->v};
+        CSD_CU(csd::dev::gemm_tc_proj(x_in, w, o, 3, B * N, D, Dl, nullptr, s), "gemm_tc_qkv");
+        blk->ctx->launches += 1;
+    } else {
+        CSD_TRY(csd_project(ctx, md, x_in, blk->wq, B, N, D, Dl, blk->q, stream));
+        CSD_TRY(csd_project(ctx, md, x_in, blk->wk, B, N, D, Dl, blk->k, stream));
+        CSD_TRY(csd_project(ctx, md, x_in, blk->wv, B, N, D, Dl, blk->v, stream));
+    }
     // Index sets produced inside the block are valid by construction (top-k); a static
     // pattern was validated by csd_block_step before anything ran.  Skip per-call validation.
     struct ValidateGuard {

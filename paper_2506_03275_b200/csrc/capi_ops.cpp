@@ -82,6 +82,19 @@ csd_status prod_dense_mlp(Ctx* c, const void* x, const void* w1, const float* b1
                           int64_t chunk, float* out, void* act_cm, const void* x_mid, void* x_out,
                           cudaStream_t s) {
     const int64_t rows = batch * n;
+    if (gemm_tc_enabled() && gemm_tc_mlp_supported(d, f, chunk)) {
+        // hand-written tcgen05 GEMMs (gemm_tc.cu): GEMM1 writes gelu(x W1^T + b1) straight
+        // into the chunk-major cache, GEMM2 reads it and writes M_cache (+b2) and x_out
+        if (!act_cm) {
+            act_cm = c->ws(kWsScores, 2 * rows * f, s);
+            CSD_TRY(need_ws(act_cm));
+        }
+        CSD_CU(gemm_tc_mlp_up(x, w1, b1, batch * (n / chunk), chunk, d, f, act_cm, s), "gemm_tc_mlp_up");
+        CSD_CU(gemm_tc_mlp_down(act_cm, w2, b2, batch * (n / chunk), chunk, d, f, out, x_mid, x_out, s),
+               "gemm_tc_mlp_down");
+        c->launches += 2;
+        return CSD_OK;
+    }
     // chunk <= 256: GELU writes only the chunk-major cache and GEMM2 runs per chunk over it
     // (saves the [rows, F] row-major activation write); otherwise the row-major path
     const bool from_cm = chunk <= 256;
@@ -416,8 +429,16 @@ csd_status csd_project(csd_ctx* ctx, csd_mode mode, const void* x, const void* w
     if (batch < 1 || n < 1 || d < 1 || dout < 1)
         return set_error(CSD_ERR_SHAPE, "project expects [B x N x D] input");
     const cudaStream_t s = S(stream);
-    if (mode == CSD_MODE_PROD)
+    if (mode == CSD_MODE_PROD) {
+        if (gemm_tc_enabled() && gemm_tc_proj_supported(batch * n, d, dout)) {
+            const void* ws[3] = {w, w, w};
+            void* os[3] = {out, out, out};
+            CSD_CU(gemm_tc_proj(x, ws, os, 1, batch * n, d, dout, nullptr, s), "gemm_tc_proj");
+            c->launches += 1;
+            return CSD_OK;
+        }
         return csd::gemm_bf16(c, x, w, false, out, false, batch * n, dout, d, 0.0f, s);
+    }
     CSD_CU(check_project((const float*)x, (const float*)w, batch, n, d, dout, (float*)out, s),
            "project");
     c->launches += 1;

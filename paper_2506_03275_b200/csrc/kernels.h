@@ -106,6 +106,21 @@ bool attn_tc_supported(int64_t e, int64_t chunk);
 bool attn_pp_supported(const AttnTcArgs& a);
 cudaError_t attn_pp(const AttnTcArgs& a, cudaStream_t s);
 
+// gemm_tc.cu: persistent tcgen05 GEMMs with fused epilogues (projections, dense MLP).
+// gemm_tc_enabled() is false when CSD_GEMM=cublas (A/B comparison against the library).
+bool gemm_tc_enabled();
+bool gemm_tc_proj_supported(int64_t rows, int64_t k, int64_t n);
+// out_i[rows, n] = x[rows, k] @ w_i[k, n] for nw weights (one launch); with resid (nw = 1):
+// out = resid + x @ w
+cudaError_t gemm_tc_proj(const void* x, const void* const w[3], void* const out[3], int nw,
+                         int64_t rows, int64_t k, int64_t n, const void* resid, cudaStream_t s);
+bool gemm_tc_mlp_supported(int64_t d, int64_t f, int64_t chunk);
+cudaError_t gemm_tc_mlp_up(const void* x, const void* w1, const float* b1, int64_t chunks,
+                           int64_t chunk, int64_t d, int64_t f, void* cm, cudaStream_t s);
+cudaError_t gemm_tc_mlp_down(const void* cm, const void* w2, const float* b2, int64_t chunks,
+                             int64_t chunk, int64_t d, int64_t f, float* mcache,
+                             const void* x_mid, void* x_out, cudaStream_t s);
+
 cudaError_t prod_cast_f32_bf16(const float* in, void* out, int64_t n, cudaStream_t s);
 cudaError_t prod_cast_bf16_f32(const void* in, float* out, int64_t n, cudaStream_t s);
 

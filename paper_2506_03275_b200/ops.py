@@ -393,6 +393,20 @@ def dense_mlp(x, w: MlpWeights, chunk: int = 0):
     return out, act
 
 
+def project(x, w) -> torch.Tensor:
+    """model.cpp:107-120: [B, N, D] @ [D, Dout] -> [B, N, Dout] (PROD: the tcgen05 GEMM of
+    gemm_tc.cu, bf16 out; CHECK: float32, the reference's loop order)."""
+    from .errors import ShapeError
+    if x.dim() != 3:
+        raise ShapeError(f"project expects [B x N x D] input, got {list(x.shape)}")
+    if w.dim() != 2 or w.shape[0] != x.shape[2]:
+        raise ShapeError(f"project weight {list(w.shape)} does not match input dim {x.shape[2]}")
+    b, n, d = x.shape
+    out = torch.empty((b, n, w.shape[1]), dtype=x.dtype, device=x.device)
+    _call("csd_project", _mode(x), _ptr(x), _ptr(w), b, n, d, w.shape[1], _ptr(out), _stream())
+    return out
+
+
 def mlp_tile_means(x, w1, chunk: int) -> torch.Tensor:
     """mlp.cpp:83-96"""
     from .errors import ShapeError
