@@ -444,6 +444,9 @@ def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps, dense_ms=None, flus
     t_sparse = timed(lambda: ops.sparse_delta_attention(q, k, v, idx, base, 1.0, layout=1, out=out))
     ops.context().set_validation(True)
     t_dense = dense_ms if dense_ms is not None else timed(lambda: ops.dense_attention(q, k, v, layout=1))
+    # the dense STEP's pass: dense attention + stale-stat chunk column sums (attention.cpp:76-145)
+    stats = r.stats
+    t_colsum = timed(lambda: ops.column_sum_attention(q, k, v, stats, c, layout=1))
     elem = 2
     alg_bytes = 5 * n * h * e * elem  # Q, K, V, base, out
     gather_bytes = 2 * h * (n // c) * (((attn_k + 3) // 4) * 4) * e * elem  # K + V rows, 4-row groups
@@ -455,6 +458,7 @@ def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps, dense_ms=None, flus
                        "dense_equiv_tflops": round(dense_flops / (t_sparse * 1e-3) / 1e12, 2)},
             "dense": {"ms": round(t_dense, 5), "flops": dense_flops,
                       "tflops": round(dense_flops / (t_dense * 1e-3) / 1e12, 2)},
+            "colsum": {"ms": round(t_colsum, 5), "vs_dense": round(t_colsum / t_dense, 3)},
             "speedup_vs_dense": round(t_dense / t_sparse, 3),
             "k": attn_k, "n": n, "reps": reps,
             "l2_flush": "256 MB write between reps" if flush_l2 else "none (L2 warm)"}

@@ -104,6 +104,10 @@ bool attn_tc_supported(int64_t e, int64_t chunk);
 // attn_pp.cu: ping-pong-tile kernel for items of 129..256 rows without column sums
 // (CSD_ATTN_KERNEL=tc forces k_attn_tc); attn_tc() dispatches to it.
 bool attn_pp_supported(const AttnTcArgs& a);
+// attn_sd.cu: dense passes (dense attention, stats, stale-stat column sums) with a
+// double-buffered S and tensor-core column sums; attn_tc() dispatches to it first.
+bool attn_sd_supported(const AttnTcArgs& a);
+cudaError_t attn_sd(const AttnTcArgs& a, cudaStream_t s);
 cudaError_t attn_pp(const AttnTcArgs& a, cudaStream_t s);
 
 // gemm_tc.cu: persistent tcgen05 GEMMs with fused epilogues (projections, dense MLP).
