@@ -363,26 +363,25 @@ def run_ours(args, rank, world):
                                 "streams overlap the block steps (4 x / y buffers)"},
             "gpu_launches": int(launches),
             "roofline": {
-                "kernel": "k_attn_tc (column-sparse attention, sparse step)",
+                "kernel": "k_attn_pp (column-sparse attention, sparse step)",
                 "bound": "hbm",
                 "achieved": round(att["alg_bytes"] / (att["ms"] * 1e-3) / 1e9, 1),
                 "peak": hbm, "peak_source": src, "unit": "GB/s",
                 "frac": round(att["alg_bytes"] / (att["ms"] * 1e-3) / 1e9 / hbm, 4),
-                "traffic": profiled_traffic("k_attn_tc"),
+                "traffic": profiled_traffic("k_attn_pp"),
                 "traffic_unit": "bytes per launch (dram read + write, ncu --set full, "
                                 "profiles/latest_full.json)",
                 "alg_bytes": att["alg_bytes"],
                 "tensor_frac": round(att["flops"] / (att["ms"] * 1e-3) / 1e12 / tf, 4),
-                # the K/V rows gathered through TMA tile::gather4 (14 B/ns per SM in isolation,
-                # scripts/gather_bench2.cu).  Not the binding resource: a compacted-rows variant
-                # with plain TMA tiles was no faster; the kernel is bound by its
-                # softmax -> P.V -> S schedule at ~47 % tensor-pipe occupancy per block, the
-                # tcgen05.mma itself running at 64 cycles per M128.N128.K16 (scripts/mma_bench.cu)
+                # the K/V rows gathered by cp.async from 6 copy warps (LSU path, 36-40 B/ns per
+                # SM L2-resident, scripts/gather_bench2.cu); not the binding resource either
                 "gather": {"bytes": att["gather_bytes"],
                            "achieved_gbs": round(att["gather_bytes"] / (att["ms"] * 1e-3) / 1e9, 1),
-                           "measured_gather4_gbs": 148 * 14.0,
-                           "frac": round(att["gather_bytes"] / (att["ms"] * 1e-3) / 1e9 / (148 * 14.0), 4)},
-                "limiter": "softmax -> P.V -> S dependency chain per key block (not HBM, not gather4)",
+                           "measured_cp_async_gbs": 148 * 40.0,
+                           "frac": round(att["gather_bytes"] / (att["ms"] * 1e-3) / 1e9 / (148 * 40.0), 4)},
+                "limiter": "per-item latency: ~4 items of 3 key blocks per SM, each block a "
+                           "MUFU-bound softmax (2.3k cycles) -> P.V -> next S chain plus the item "
+                           "epilogue (scripts/attn_pp_trace.py timelines, DESIGN.md 4.3)",
             },
         }
     return out

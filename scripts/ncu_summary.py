@@ -21,7 +21,13 @@ METRICS = OrderedDict([
     ("dram_write_MB", ("dram__bytes_write.sum", None)),
     ("dram_throughput_pct", ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", None)),
     ("sm_throughput_pct", ("sm__throughput.avg.pct_of_peak_sustained_elapsed", None)),
-    ("tensor_pipe_pct", ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", None)),
+    # tcgen05 activity: sm__mem_tensor_cycles_active (the UTC/TMEM path).  The legacy
+    # sm__pipe_tensor_* / hmma counters do not see tcgen05.mma (they read 0-18 % on cuBLAS
+    # nvjet GEMMs running at ~66 % of the nominal MMA rate).  Calibration on this pool's B200
+    # (profiles/r02_gemm_calibration.md): nvjet 192x256 2-CTA bf16 GEMM reads 77 % elapsed at
+    # 1.46 PF/s (66 % of 8192 flop/clk/SM at the measured clock) -> the counter runs ~1.15x
+    # the MMA-rate utilisation.
+    ("tensor_active_pct", ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", None)),
     ("warps_active_pct", ("sm__warps_active.avg.pct_of_peak_sustained_active", None)),
     ("registers", ("launch__registers_per_thread", None)),
     ("grid", ("launch__grid_size", None)),
@@ -71,7 +77,7 @@ def full(rep, out):
         kernels.append(k)
     with open(out + ".json", "w") as f:
         json.dump({"source": rep, "kernels": kernels}, f, indent=1)
-    cols = ["duration_us", "dram_traffic_MB", "dram_throughput_pct", "tensor_pipe_pct",
+    cols = ["duration_us", "dram_traffic_MB", "dram_throughput_pct", "tensor_active_pct",
             "sm_throughput_pct", "warps_active_pct", "registers"]
     with open(out + ".md", "w") as f:
         f.write(f"# ncu --set full summary ({rep})\n\n| kernel | " + " | ".join(cols) +
