@@ -138,11 +138,16 @@ def run_ours(args, rank, world):
                          head_dim=cfg["head_dim"], hidden=cfg["hidden"], chunk=cfg["chunk"],
                          attn_k=attn_k, mlp_k=mlp_k)
     sharded = world > 1 or args.sharded
-    if sharded:
+    if sharded and args.shard_mode == "column":
         # heads + MLP hidden columns over the ranks; NCCL all-reduce of the Wo / W2 partials
         # and all-gather of the MLP selection candidates (paper_2506_03275_b200/shard.py)
         from paper_2506_03275_b200.shard import ShardedBlock, TorchComm
         blk = ShardedBlock(bc, make_weights(cfg), TorchComm())
+    elif sharded:
+        # token-sharded: attention by heads, one bf16 all-to-all to token rows, Wo + MLP on
+        # this rank's rows, one bf16 all-gather of the output rows
+        from paper_2506_03275_b200.shard import TokenShardedBlock, TorchComm
+        blk = TokenShardedBlock(bc, make_weights(cfg), TorchComm())
     else:
         blk = ops.Block(bc, make_weights(cfg), production=True)
     ctx = ops.context()
@@ -344,8 +349,11 @@ def run_ours(args, rank, world):
                 "heads": cfg["heads"], "head_dim": cfg["head_dim"], "mlp_hidden": cfg["hidden"],
                 "chunk": cfg["chunk"], "voxel": list(cfg["voxel"]), "sparsity": cfg["sparsity"],
                 "attn_k": attn_k, "mlp_k": mlp_k, "dense_interval": args.dense_interval,
-                "parallelism": (f"heads/{world} + mlp-columns/{world}, NCCL all-reduce + "
-                                f"all-gather" if sharded else "single-gpu"),
+                "parallelism": ("single-gpu" if not sharded else
+                                (f"heads/{world} + mlp-columns/{world}, NCCL all-reduce + all-gather"
+                                 if args.shard_mode == "column" else
+                                 f"attention heads/{world}, Wo + MLP token rows/{world}; NCCL bf16 "
+                                 f"all-to-all + all-gather")),
                 "l2": "step inputs (x + 226 MB bf16 weights) exceed the 126 MB L2; attention "
                       "kernel reps flush L2 with a 256 MB write",
                 "inputs": "22-latent generation trajectory (x <- x + y/50 from the seeded "
@@ -641,6 +649,9 @@ def main():
     ap.add_argument("--dense-interval", type=int, default=10)
     ap.add_argument("--kernel-reps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard-mode", default="token", choices=["token", "column"],
+                    help="multi-rank decomposition: token rows after the head-sharded attention "
+                         "(bf16 all-to-all + all-gather) or MLP hidden columns (fp32 all-reduces)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded block path even at one rank (runs under torchrun)")
     args = ap.parse_args()

@@ -224,6 +224,9 @@ typedef struct {
     int64_t batch, seq, dim, heads, head_dim, hidden, chunk;
     int64_t attn_k, mlp_k;   /* per-chunk keys / neurons recomputed */
     int64_t head0, heads_local, f0, f_local;  /* shard (0, heads, 0, hidden) = whole block */
+    /* token-sharded execution: this rank's output projection and MLP run on token rows
+     * [t0, t0 + t_local) of the B*N rows (chunk-aligned); 0, 0 = not token-sharded */
+    int64_t t0, t_local;
 } csd_block_config;
 
 typedef struct csd_block csd_block;
@@ -269,6 +272,19 @@ csd_status csd_block_mlp_candidates(csd_block* blk, const void* x_mid, float* ca
 csd_status csd_block_mlp_sparse_partial(csd_block* blk, const void* x_mid,
                                         const float* all_scores, const int32_t* all_ids,
                                         int64_t world, float* mlp_partial, void* stream);
+/* ---- Token-sharded execution (PROD, csd_block_config.t_local > 0): attention
+ * by heads, the output projection and the MLP by token rows; the caller's collectives move
+ * bf16 only.  One step on rank r of g (equal heads per rank, equal chunk-aligned rows):
+ *   csd_block_attn_heads(x_in [B*N, D] -> attn_local [B*N, heads_local*E])
+ *   all-to-all: rows [t0_s, +t_local) of attn_local to rank s   -> attn_rows [g][t_local][Dl]
+ *   csd_block_rows_step(x_in rows [t0, +t_local), attn_rows, g -> x_out rows)
+ *   all-gather x_out rows in rank order                         -> x_out [B*N, D]
+ * The MLP selection and caches are per chunk, so the rows step is exactly the single-GPU
+ * step on those rows (weights wo / w1 / w2 replicated). */
+csd_status csd_block_attn_heads(csd_block* blk, const void* x_in, int dense, void* attn_local,
+                                void* stream);
+csd_status csd_block_rows_step(csd_block* blk, const void* x_rows, const void* attn_rows,
+                               int64_t world, int dense, void* x_out_rows, void* stream);
 /* out_bf16 = bf16(x_bf16 + partial_f32) (PROD residual after an all-reduce). */
 csd_status csd_residual_add(csd_ctx* ctx, const void* x, const float* partial, int64_t numel,
                             void* out, void* stream);

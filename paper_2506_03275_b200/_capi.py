@@ -29,7 +29,7 @@ fp = C.c_void_p  # device pointers are passed as integers / void*
 class BlockConfig(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "batch", "seq", "dim", "heads", "head_dim", "hidden", "chunk", "attn_k", "mlp_k",
-        "head0", "heads_local", "f0", "f_local")]
+        "head0", "heads_local", "f0", "f_local", "t0", "t_local")]
 
 
 # name -> (restype, [argtypes])
@@ -71,6 +71,8 @@ SIGNATURES = {
     "csd_block_step": (i32, [p, fp, fp, C.c_int, fp, fp, i64, p]),
     "csd_block_cache": (i32, [p, C.c_int, fp, fp, p]),
     "csd_block_attn_partial": (i32, [p, fp, C.c_int, fp, p]),
+    "csd_block_attn_heads": (i32, [p, fp, C.c_int, fp, p]),
+    "csd_block_rows_step": (i32, [p, fp, fp, i64, C.c_int, fp, p]),
     "csd_block_mlp_dense_partial": (i32, [p, fp, fp, p]),
     "csd_block_mlp_candidates": (i32, [p, fp, fp, fp, p]),
     "csd_block_mlp_sparse_partial": (i32, [p, fp, fp, fp, i64, fp, p]),

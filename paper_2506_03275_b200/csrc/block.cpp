@@ -56,6 +56,9 @@ struct csd_block {
     int32_t *midx = nullptr, *mcnt = nullptr;
     bool attn_init = false, mlp_init = false;
     int64_t attn_age = 0, mlp_age = 0;
+    // the MLP's view of the rows: (batch, seq) of the block, or (1, t_local) when token-sharded
+    int64_t mB = 0, mN = 0;
+    bool token_mode = false;
 
     void* alloc(size_t bytes) {
         void* p = nullptr;
@@ -125,6 +128,17 @@ csd_status csd_block_create(csd_ctx* ctx, csd_mode mode, const csd_block_config*
                          (long long)c.seq, (long long)c.chunk);
     if (c.head0 < 0 || c.head0 + c.heads_local > c.heads || c.f0 < 0 || c.f0 + c.f_local > c.hidden)
         return set_error(CSD_ERR_CONFIG, "shard outside the block");
+    const bool token_mode = c.t_local > 0;
+    if (token_mode) {
+        // token rows are whole chunks (chunks never straddle sequences: seq % chunk == 0)
+        if (mode != CSD_MODE_PROD)
+            return set_error(CSD_ERR_UNSUPPORTED, "token-sharded blocks are PROD only");
+        if (c.t0 < 0 || c.t0 % c.chunk || c.t_local % c.chunk || c.t0 + c.t_local > c.batch * c.seq)
+            return set_error(CSD_ERR_CONFIG, "token rows [%lld, +%lld) not chunk-aligned inside the block",
+                             (long long)c.t0, (long long)c.t_local);
+        if (c.f0 != 0 || c.f_local != c.hidden)
+            return set_error(CSD_ERR_CONFIG, "token-sharded blocks keep every hidden neuron");
+    }
     auto* blk = new csd_block;
     blk->ctx = reinterpret_cast<Ctx*>(ctx);
     blk->mode = mode;
@@ -140,7 +154,9 @@ csd_status csd_block_create(csd_ctx* ctx, csd_mode mode, const csd_block_config*
     if ((st = upload(blk, &blk->wq, wq, D, Dl, D, 0, col0, false)) != CSD_OK) return fail(st);
     if ((st = upload(blk, &blk->wk, wk, D, Dl, D, 0, col0, false)) != CSD_OK) return fail(st);
     if ((st = upload(blk, &blk->wv, wv, D, Dl, D, 0, col0, false)) != CSD_OK) return fail(st);
-    if ((st = upload(blk, &blk->wo, wo, Dl, D, D, col0, 0, false)) != CSD_OK) return fail(st);
+    // output projection: this shard's head rows of Wo, or all of it for token rows
+    if ((st = upload(blk, &blk->wo, wo, token_mode ? D : Dl, D, D, token_mode ? 0 : col0, 0, false)) != CSD_OK)
+        return fail(st);
     if ((st = upload(blk, &blk->w1, w1, Fl, D, D, c.f0, 0, false)) != CSD_OK) return fail(st);
     if ((st = upload(blk, &blk->w2, w2, Fl, D, D, c.f0, 0, false)) != CSD_OK) return fail(st);
     void* tmp = nullptr;
@@ -151,13 +167,17 @@ csd_status csd_block_create(csd_ctx* ctx, csd_mode mode, const csd_block_config*
     if ((st = upload(blk, &tmp, b2l.data(), 1, D, D, 0, 0, true)) != CSD_OK) return fail(st);
     blk->b2 = (float*)tmp;
 
+    blk->token_mode = token_mode;
+    blk->mB = token_mode ? 1 : B;
+    blk->mN = token_mode ? c.t_local : N;
+    const int64_t MR = blk->mB * blk->mN, MC = MR / c.chunk;  // MLP rows / chunks
     const size_t es = esz(mode);
     blk->q = blk->alloc(es * B * N * Dl);
     blk->k = blk->alloc(es * B * N * Dl);
     blk->v = blk->alloc(es * B * N * Dl);
     blk->attn = blk->alloc(es * B * N * Dl);
     blk->resid = blk->alloc(es * B * N * Dl);
-    blk->x_mid = blk->alloc(es * B * N * D);
+    blk->x_mid = blk->alloc(es * (token_mode ? MR : B * N) * D);
     blk->proj = (float*)blk->alloc(4 * B * N * D);
     for (int i = 0; i < 2; ++i) {
         blk->m[i] = (float*)blk->alloc(4 * B * Hl * N);
@@ -168,12 +188,13 @@ csd_status csd_block_create(csd_ctx* ctx, csd_mode mode, const csd_block_config*
     blk->a_kmax = ak;
     blk->aidx = (int32_t*)blk->alloc(4 * B * Hl * C * ak);
     blk->acnt = (int32_t*)blk->alloc(4 * B * Hl * C);
-    blk->tmeans = (float*)blk->alloc(4 * B * C * Fl);
-    blk->act = blk->alloc(es * B * N * Fl);
-    blk->mout = (float*)blk->alloc(4 * B * N * D);
+    blk->tmeans = (float*)blk->alloc(4 * MC * Fl);
+    blk->act = blk->alloc(es * MR * Fl);
+    blk->mout = (float*)blk->alloc(4 * MR * D);
     const int64_t mk = c.mlp_k > 0 ? c.mlp_k : Fl;
-    blk->midx = (int32_t*)blk->alloc(4 * B * C * mk);
-    blk->mcnt = (int32_t*)blk->alloc(4 * B * C);
+    blk->midx = (int32_t*)blk->alloc(4 * MC * mk);
+    blk->mcnt = (int32_t*)blk->alloc(4 * MC);
+    (void)C;
     for (void* p : blk->allocs)
         if (!p) return fail(set_error(CSD_ERR_CUDA, "block allocation failed"));
     *out = blk;
@@ -200,6 +221,8 @@ csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int den
                           const int32_t* static_idx, const int32_t* static_counts,
                           int64_t static_k_max, void* stream) {
     if (!blk) return set_error(CSD_ERR_VALUE, "null block");
+    if (blk->token_mode)
+        return set_error(CSD_ERR_UNSUPPORTED, "token-sharded block: use csd_block_attn_heads / csd_block_rows_step");
     const auto& c = blk->cfg;
     csd_ctx* ctx = reinterpret_cast<csd_ctx*>(blk->ctx);
     const csd_mode md = blk->mode;
@@ -368,7 +391,7 @@ static csd_status attn_core(csd_block* blk, const void* x_in, int dense, const i
 // fused residual x_out = x_mid + M_cache.
 static csd_status sparse_mlp_apply(csd_block* blk, const void* x_mid, void* x_out, cudaStream_t s) {
     const auto& c = blk->cfg;
-    const int64_t B = c.batch, N = c.seq, D = c.dim, Fl = c.f_local;
+    const int64_t B = blk->mB, N = blk->mN, D = c.dim, Fl = c.f_local;
     const int64_t mk = c.mlp_k > 0 ? c.mlp_k : Fl;
     if (!mlp_tc_supported(D, c.chunk))
         return set_error(CSD_ERR_UNSUPPORTED, "sparse-delta MLP envelope (D %% 128, chunk <= 256)");
@@ -467,6 +490,57 @@ csd_status csd_block_mlp_sparse_partial(csd_block* blk, const void* x_mid,
     return CSD_OK;
 }
 
+// ---------------------------------------------------------------- token-sharded execution
+csd_status csd_block_attn_heads(csd_block* blk, const void* x_in, int dense, void* attn_local,
+                                void* stream) {
+    if (!blk || !x_in || !attn_local) return set_error(CSD_ERR_VALUE, "null argument");
+    if (blk->mode != CSD_MODE_PROD) return set_error(CSD_ERR_UNSUPPORTED, "sharded steps are PROD only");
+    if (!dense && !blk->attn_init)
+        return set_error(CSD_ERR_STATE, "sparse attention step requested before any dense step");
+    // the attention output lands in the caller's buffer (the block's attn buffer is not a cache)
+    void* own = blk->attn;
+    blk->attn = attn_local;
+    const csd_status st = attn_core(blk, x_in, dense, nullptr, nullptr, 0, stream);
+    blk->attn = own;
+    return st;
+}
+
+csd_status csd_block_rows_step(csd_block* blk, const void* x_rows, const void* attn_rows,
+                               int64_t world, int dense, void* x_out_rows, void* stream) {
+    if (!blk || !x_rows || !attn_rows || !x_out_rows) return set_error(CSD_ERR_VALUE, "null argument");
+    if (!blk->token_mode) return set_error(CSD_ERR_STATE, "block is not token-sharded (t_local == 0)");
+    const auto& c = blk->cfg;
+    const int64_t R = c.t_local, D = c.dim, Dl = c.heads_local * c.head_dim, Fl = c.f_local;
+    if (world < 1 || world * Dl != D)
+        return set_error(CSD_ERR_SHAPE, "token rows need equal head shards: world %lld x %lld != dim %lld",
+                         (long long)world, (long long)Dl, (long long)D);
+    if (!dense && !blk->mlp_init)
+        return set_error(CSD_ERR_STATE, "sparse MLP step requested before any dense step");
+    csd_ctx* ctx = reinterpret_cast<csd_ctx*>(blk->ctx);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t mk = c.mlp_k > 0 ? c.mlp_k : Fl;
+    // x_mid = x + O Wo over the rank-blocked head outputs [world][R][Dl] (the all-to-all's
+    // layout: the GEMM's A operand walks the blocks, no re-layout copy)
+    if (!csd::dev::gemm_tc_enabled() || !csd::dev::gemm_tc_proj_supported(R, D, D) || Dl % 64)
+        return set_error(CSD_ERR_UNSUPPORTED, "token rows: tcgen05 projection envelope (rows %% 128, dims %% 64)");
+    CSD_CU(csd::dev::gemm_tc_proj_blocked(attn_rows, blk->wo, blk->x_mid, R, D, D, x_rows, Dl, R, s),
+           "gemm_tc_wo_rows");
+    blk->ctx->launches += 1;
+    if (dense) {
+        CSD_TRY(csd::prod_dense_mlp(blk->ctx, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, 1, R, D,
+                                    Fl, c.chunk, blk->mout, blk->act, blk->x_mid, x_out_rows, s));
+        CSD_TRY(csd_mlp_tile_means(ctx, blk->mode, blk->x_mid, blk->w1, 1, R, D, Fl, c.chunk,
+                                   blk->tmeans, stream));
+        blk->mlp_init = true;
+        blk->mlp_age = 0;
+    } else {
+        CSD_TRY(csd_mlp_change_indices(ctx, blk->mode, blk->x_mid, blk->w1, blk->tmeans, 1, R, D, Fl,
+                                       mk, c.chunk, blk->midx, blk->mcnt, stream));
+        CSD_TRY(sparse_mlp_apply(blk, blk->x_mid, x_out_rows, s));
+    }
+    return CSD_OK;
+}
+
 csd_status csd_residual_add(csd_ctx* ctx, const void* x, const float* partial, int64_t numel,
                             void* out, void* stream) {
     CSD_CU(prod_add_bf16_f32(x, partial, numel, out, static_cast<cudaStream_t>(stream)), "add");
@@ -481,6 +555,8 @@ csd_status csd_block_cache(csd_block* blk, int which, void* out, int32_t* counts
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t B = c.batch, N = c.seq, D = c.dim, E = c.head_dim, Hl = c.heads_local;
     const int64_t Fl = c.f_local, C = N / c.chunk;
+    // the MLP caches cover the block's MLP rows (all of B x N, or the token shard's rows)
+    const int64_t MB = blk->mB, MN = blk->mN, MC = MN / c.chunk;
     csd_ctx* ctx = reinterpret_cast<csd_ctx*>(blk->ctx);
     switch (which) {
         case 0: {  // residual [B,H,N,E] fp32 from token-major storage
@@ -511,13 +587,13 @@ csd_status csd_block_cache(csd_block* blk, int which, void* out, int32_t* counts
             CSD_CU(cudaMemcpyAsync(out, blk->l[blk->cur], 4 * B * Hl * N, cudaMemcpyDeviceToDevice, s), "copy");
             return CSD_OK;
         case 3:
-            return csd_mlp_act_cache_to_ref(ctx, blk->mode, blk->act, B, N, Fl, c.chunk, (float*)out,
+            return csd_mlp_act_cache_to_ref(ctx, blk->mode, blk->act, MB, MN, Fl, c.chunk, (float*)out,
                                             stream);
         case 4:
-            CSD_CU(cudaMemcpyAsync(out, blk->mout, 4 * B * N * D, cudaMemcpyDeviceToDevice, s), "copy");
+            CSD_CU(cudaMemcpyAsync(out, blk->mout, 4 * MB * MN * D, cudaMemcpyDeviceToDevice, s), "copy");
             return CSD_OK;
         case 5:
-            CSD_CU(cudaMemcpyAsync(out, blk->tmeans, 4 * B * C * Fl, cudaMemcpyDeviceToDevice, s), "copy");
+            CSD_CU(cudaMemcpyAsync(out, blk->tmeans, 4 * MB * MC * Fl, cudaMemcpyDeviceToDevice, s), "copy");
             return CSD_OK;
         case 6:
             CSD_CU(cudaMemcpyAsync(out, blk->aidx, 4 * B * Hl * C * blk->a_kmax, cudaMemcpyDeviceToDevice, s), "copy");
@@ -526,9 +602,9 @@ csd_status csd_block_cache(csd_block* blk, int which, void* out, int32_t* counts
             return CSD_OK;
         case 7: {
             const int64_t mk = c.mlp_k > 0 ? c.mlp_k : Fl;
-            CSD_CU(cudaMemcpyAsync(out, blk->midx, 4 * B * C * mk, cudaMemcpyDeviceToDevice, s), "copy");
+            CSD_CU(cudaMemcpyAsync(out, blk->midx, 4 * MB * MC * mk, cudaMemcpyDeviceToDevice, s), "copy");
             if (counts_out)
-                CSD_CU(cudaMemcpyAsync(counts_out, blk->mcnt, 4 * B * C, cudaMemcpyDeviceToDevice, s), "copy");
+                CSD_CU(cudaMemcpyAsync(counts_out, blk->mcnt, 4 * MB * MC, cudaMemcpyDeviceToDevice, s), "copy");
             return CSD_OK;
         }
     }

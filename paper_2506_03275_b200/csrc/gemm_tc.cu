@@ -67,6 +67,7 @@ struct GemmParams {
     __nv_bfloat16* xout;         // kEpiMlpOut: x_out = x_mid + M_cache (nullable)
     int m_total;                 // M (rows of A / leading dim of the MLP-out outputs)
     int chunk;                   // A from the chunk-major cache: rows per chunk
+    int a_bk, a_brows;           // K-major A in column blocks of a_bk, stacked by rows (0: plain)
 };
 
 // Epilogue of one thread: 32-column chunks r[c * 32 ..] of tile row `m` (TMEM lane), tile
@@ -260,7 +261,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUte
                     uint8_t* a_dst = sa + s * p.a_stage;
                     uint8_t* b_dst = sb + s * p.b_stage;
                     if (!AMN) {
-                        tma_load_2d(&tm_a, full + s, a_dst, kb * 64, mt * 128);
+                        if (p.a_bk > 0)  // block (kb * 64) / a_bk of the row-stacked A
+                            tma_load_2d(&tm_a, full + s, a_dst, (kb * 64) % p.a_bk,
+                                        ((kb * 64) / p.a_bk) * p.a_brows + mt * 128);
+                        else
+                            tma_load_2d(&tm_a, full + s, a_dst, kb * 64, mt * 128);
                     } else {
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
@@ -421,7 +426,11 @@ k_gemm2_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUt
                     uint8_t* a_dst = sa + s * p.a_stage;
                     uint8_t* b_dst = sb + s * p.b_stage;
                     if (!ACM) {
-                        tma_load_2d_pair(&tm_a, full + s, a_dst, kb * 64, m_cta);
+                        if (p.a_bk > 0)
+                            tma_load_2d_pair(&tm_a, full + s, a_dst, (kb * 64) % p.a_bk,
+                                             ((kb * 64) / p.a_bk) * p.a_brows + m_cta);
+                        else
+                            tma_load_2d_pair(&tm_a, full + s, a_dst, kb * 64, m_cta);
                     } else {
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
@@ -608,12 +617,17 @@ static int proj_bn(int64_t n) {
 
 // q|k|v[rows, n] = x[rows, k] @ {wq, wk, wv}[k, n]  (any of the outputs may be null: fewer
 // weights); one launch.
-cudaError_t gemm_tc_proj(const void* x, const void* const w[3], void* const out[3], int nw,
-                         int64_t rows, int64_t k, int64_t n, const void* resid, cudaStream_t s) {
+static cudaError_t gemm_tc_proj_impl(const void* x, const void* const w[3], void* const out[3],
+                                     int nw, int64_t rows, int64_t k, int64_t n, const void* resid,
+                                     int64_t a_bk, cudaStream_t s) {
     if (!gemm_tc_proj_supported(rows, k, n) || nw < 1 || nw > 3) return cudaErrorNotSupported;
+    if (a_bk > 0 && (a_bk % 64 || k % a_bk)) return cudaErrorNotSupported;
     const int bn = proj_bn(n);
     CUtensorMap ta, tb[3];
-    if (!map_box(&ta, x, k, rows, k, 64, 128)) return cudaErrorInvalidValue;
+    // plain A [rows][k], or k / a_bk column blocks of width a_bk stacked by rows
+    if (a_bk > 0 ? !map_box(&ta, x, a_bk, (k / a_bk) * rows, a_bk, 64, 128)
+                 : !map_box(&ta, x, k, rows, k, 64, 128))
+        return cudaErrorInvalidValue;
     for (int i = 0; i < 3; ++i)
         if (!map_box(&tb[i], w[i < nw ? i : 0], n, k, n, 64, 64)) return cudaErrorInvalidValue;
     GemmParams p{};
@@ -629,6 +643,8 @@ cudaError_t gemm_tc_proj(const void* x, const void* const w[3], void* const out[
     p.out2 = static_cast<__nv_bfloat16*>(out[nw > 2 ? 2 : 0]);
     p.resid = static_cast<const __nv_bfloat16*>(resid);
     p.m_total = (int)rows;
+    p.a_bk = (int)a_bk;
+    p.a_brows = (int)rows;
     if (use_pair() && rows % 256 == 0 && bn % 128 == 0) {
         p.tiles_m = (int)(rows / 256);
         if (resid != nullptr) {
@@ -654,6 +670,22 @@ cudaError_t gemm_tc_proj(const void* x, const void* const w[3], void* const out[
         case 128: return launch_gemm<128, false, true, kEpiStore>(ta, tb[0], tb[1], tb[2], p, s);
         default: return launch_gemm<64, false, true, kEpiStore>(ta, tb[0], tb[1], tb[2], p, s);
     }
+}
+
+cudaError_t gemm_tc_proj(const void* x, const void* const w[3], void* const out[3], int nw,
+                         int64_t rows, int64_t k, int64_t n, const void* resid, cudaStream_t s) {
+    return gemm_tc_proj_impl(x, w, out, nw, rows, k, n, resid, 0, s);
+}
+
+// out[rows, n] = resid + A @ w with A given as k / a_bk column blocks [k / a_bk][rows][a_bk]
+// (the head-sharded attention outputs after the token all-to-all)
+cudaError_t gemm_tc_proj_blocked(const void* a_blocks, const void* w, void* out, int64_t rows,
+                                 int64_t k, int64_t n, const void* resid, int64_t a_bk,
+                                 int64_t a_brows, cudaStream_t s) {
+    if (a_brows != rows) return cudaErrorInvalidValue;
+    const void* ws[3] = {w, w, w};
+    void* os[3] = {out, out, out};
+    return gemm_tc_proj_impl(a_blocks, ws, os, 1, rows, k, n, resid, a_bk, s);
 }
 
 bool gemm_tc_mlp_supported(int64_t d, int64_t f, int64_t chunk) {

@@ -118,6 +118,9 @@ bool gemm_tc_proj_supported(int64_t rows, int64_t k, int64_t n);
 // out = resid + x @ w
 cudaError_t gemm_tc_proj(const void* x, const void* const w[3], void* const out[3], int nw,
                          int64_t rows, int64_t k, int64_t n, const void* resid, cudaStream_t s);
+cudaError_t gemm_tc_proj_blocked(const void* a_blocks, const void* w, void* out, int64_t rows,
+                                 int64_t k, int64_t n, const void* resid, int64_t a_bk,
+                                 int64_t a_brows, cudaStream_t s);
 bool gemm_tc_mlp_supported(int64_t d, int64_t f, int64_t chunk);
 cudaError_t gemm_tc_mlp_up(const void* x, const void* w1, const float* b1, int64_t chunks,
                            int64_t chunk, int64_t d, int64_t f, void* cm, cudaStream_t s);

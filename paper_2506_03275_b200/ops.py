@@ -497,6 +497,8 @@ class BlockConfig:
     heads_local: int = 0
     f0: int = 0
     f_local: int = 0
+    t0: int = 0       # token-sharded execution: Wo + MLP on rows [t0, t0 + t_local)
+    t_local: int = 0
 
 
 class Block:
@@ -551,14 +553,36 @@ class Block:
         """A fresh ModelState for this layer (model.cpp:101-105): the next step must be dense."""
         raise_for(self.ctx.lib, self.ctx.lib.csd_block_reset(self.h))
 
+    def attn_heads(self, x: torch.Tensor, dense: bool, out: Optional[torch.Tensor] = None):
+        """Token-sharded step, part 1: this block's heads over every token -> [B*N, Dl] bf16."""
+        c = self.cfg
+        hl = c.heads_local or c.heads
+        if out is None:
+            out = torch.empty((c.batch * c.seq, hl * c.head_dim), dtype=self.dtype, device=x.device)
+        raise_for(self.ctx.lib, self.ctx.lib.csd_block_attn_heads(self.h, _ptr(x), int(bool(dense)),
+                                                                  _ptr(out), _stream()))
+        return out
+
+    def rows_step(self, x_rows: torch.Tensor, attn_rows: torch.Tensor, world: int, dense: bool,
+                  out: Optional[torch.Tensor] = None):
+        """Token-sharded step, part 2: x_out rows = MLP(x + O Wo) on this block's token rows;
+        attn_rows = [world][t_local][Dl] (the all-to-all of every rank's attn_heads)."""
+        if out is None:
+            out = torch.empty_like(x_rows)
+        raise_for(self.ctx.lib, self.ctx.lib.csd_block_rows_step(
+            self.h, _ptr(x_rows), _ptr(attn_rows.contiguous()), int(world), int(bool(dense)),
+            _ptr(out), _stream()))
+        return out
+
     def cache(self, which: int) -> torch.Tensor:
         c = self.cfg
         hl = c.heads_local or c.heads
         fl = c.f_local or c.hidden
         nc = c.seq // c.chunk
+        mb, mn = (1, c.t_local) if c.t_local else (c.batch, c.seq)  # the MLP caches' rows
         shapes = {0: (c.batch, hl, c.seq, c.head_dim), 1: (c.batch, hl, c.seq),
-                  2: (c.batch, hl, c.seq), 3: (c.batch, c.seq, fl), 4: (c.batch, c.seq, c.dim),
-                  5: (c.batch, nc, fl)}
+                  2: (c.batch, hl, c.seq), 3: (mb, mn, fl), 4: (mb, mn, c.dim),
+                  5: (mb, mn // c.chunk, fl)}
         t = torch.empty(shapes[which], dtype=torch.float32, device="cuda")
         raise_for(self.ctx.lib, self.ctx.lib.csd_block_cache(self.h, which, _ptr(t), None, _stream()))
         return t
@@ -567,9 +591,11 @@ class Block:
         c = self.cfg
         hl = 1 if mlp else (c.heads_local or c.heads)
         k = (c.mlp_k or (c.f_local or c.hidden)) if mlp else (c.attn_k or c.seq)
-        nc = c.seq // c.chunk
-        idx = torch.empty((c.batch, hl, nc, k), dtype=torch.int32, device="cuda")
-        cnt = torch.empty((c.batch, hl, nc), dtype=torch.int32, device="cuda")
+        b, nc = c.batch, c.seq // c.chunk
+        if mlp and c.t_local:  # a token shard's MLP chunks
+            b, nc = 1, c.t_local // c.chunk
+        idx = torch.empty((b, hl, nc, k), dtype=torch.int32, device="cuda")
+        cnt = torch.empty((b, hl, nc), dtype=torch.int32, device="cuda")
         raise_for(self.ctx.lib, self.ctx.lib.csd_block_cache(self.h, 7 if mlp else 6, _ptr(idx),
                                                              _ptr(cnt), _stream()))
         return idx, cnt

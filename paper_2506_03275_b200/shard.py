@@ -54,7 +54,7 @@ def shard_config(cfg: BlockConfig, world: int, rank: int, f_align: int = 128) ->
 
 
 class Comm:
-    """The two collectives the sharded step needs."""
+    """The collectives the sharded steps need."""
 
     world = 1
     rank = 0
@@ -62,8 +62,17 @@ class Comm:
     def all_reduce(self, t: torch.Tensor) -> torch.Tensor:  # in place, sum
         return t
 
-    def all_gather(self, t: torch.Tensor) -> torch.Tensor:  # -> [world, *t.shape], rank order
-        return t.unsqueeze(0)
+    def all_gather(self, t: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """-> [world, *t.shape] in rank order (into `out` when given)."""
+        if out is None:
+            return t.unsqueeze(0)
+        out.view(1, *t.shape).copy_(t)
+        return out
+
+    def all_to_all(self, t: torch.Tensor) -> torch.Tensor:
+        """t = [world * rows, cols]: block s goes to rank s; returns [world, rows, cols] with
+        the block received from rank s at index s."""
+        return t.view(1, *t.shape)
 
 
 class TorchComm(Comm):
@@ -81,13 +90,21 @@ class TorchComm(Comm):
         self.dist.all_reduce(t, group=self.group)
         return t
 
-    def all_gather(self, t):
+    def all_gather(self, t, out=None):
         t = t.contiguous()
-        out = t.new_empty((self.world,) + tuple(t.shape))
+        if out is None:
+            out = t.new_empty((self.world,) + tuple(t.shape))
         if self.nccl:
             self.dist.all_gather_into_tensor(out, t, group=self.group)
         else:
             self.dist.all_gather(list(out.unbind(0)), t, group=self.group)
+        return out
+
+    def all_to_all(self, t):
+        t = t.contiguous()
+        g = self.world
+        out = t.new_empty((g, t.shape[0] // g) + tuple(t.shape[1:]))
+        self.dist.all_to_all_single(out, t, group=self.group)  # NCCL and gloo
         return out
 
 
@@ -179,6 +196,68 @@ class ShardedBlock:
         return sh.residual_add(x1, m, out)
 
 
+def token_shard_config(cfg: BlockConfig, world: int, rank: int) -> BlockConfig:
+    """Token-sharded slice: heads split evenly for attention, the B*N token rows
+    split into equal chunk-aligned ranges for Wo and the MLP (every hidden neuron)."""
+    if cfg.heads % world:
+        raise ValueError(f"{cfg.heads} heads do not split evenly over {world} ranks")
+    rows = cfg.batch * cfg.seq
+    if rows % (world * cfg.chunk):
+        raise ValueError(f"{rows} token rows do not split into {world} equal chunk-aligned ranges")
+    hl = cfg.heads // world
+    tl = rows // world
+    return replace(cfg, head0=rank * hl, heads_local=hl, f0=0, f_local=cfg.hidden,
+                   t0=rank * tl, t_local=tl)
+
+
+class TokenShardedBlock:
+    """model_forward_step for one block over a process group, token-sharded: attention by
+    heads (no communication), ONE bf16 all-to-all to token rows, Wo + the MLP on this rank's
+    rows (exact: the MLP selection is per chunk), ONE bf16 all-gather of the output rows."""
+
+    def __init__(self, cfg: BlockConfig, weights: dict, comm: Comm, block=None):
+        self.full = cfg
+        self.comm = comm
+        self.cfg = token_shard_config(cfg, comm.world, comm.rank)
+        self.block = block if block is not None else Block(self.cfg, weights, production=True)
+        c = self.cfg
+        self.rows = slice(c.t0, c.t0 + c.t_local)
+        self._attn = self._y = None  # per-step buffers, allocated on the first step (x's dtype)
+
+    def step(self, x: torch.Tensor, dense: bool, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        c, comm = self.cfg, self.comm
+        if self._attn is None or self._attn.dtype != x.dtype or self._attn.device != x.device:
+            self._attn = torch.empty((c.batch * c.seq, c.heads_local * c.head_dim), dtype=x.dtype,
+                                     device=x.device)
+            self._y = torch.empty((c.t_local, c.dim), dtype=x.dtype, device=x.device)
+        xf = x.reshape(c.batch * c.seq, c.dim)
+        a = self.block.attn_heads(xf, dense, out=self._attn)
+        a_rows = comm.all_to_all(a)  # [world, t_local, Dl]
+        y = self.block.rows_step(xf[self.rows], a_rows, comm.world, dense, out=self._y)
+        if out is None:
+            out = torch.empty_like(x)
+        comm.all_gather(y, out=out.view(comm.world, c.t_local, c.dim))
+        return out
+
+    def close(self):
+        self.block.close()
+
+
+def simulate_token_step(blocks: Sequence[Block], x: torch.Tensor, dense: bool) -> torch.Tensor:
+    """All token shards in ONE process (tests): the all-to-all / all-gather become slices and
+    concatenations in rank order; every kernel call is exactly what each rank runs."""
+    g = len(blocks)
+    c0 = blocks[0].cfg
+    xf = x.reshape(c0.batch * c0.seq, c0.dim)
+    attn = [b.attn_heads(xf, dense).clone() for b in blocks]
+    ys = []
+    for r, b in enumerate(blocks):
+        c = b.cfg
+        a_rows = torch.stack([attn[s][c.t0:c.t0 + c.t_local] for s in range(g)])
+        ys.append(b.rows_step(xf[c.t0:c.t0 + c.t_local].contiguous(), a_rows, g, dense).clone())
+    return torch.cat(ys).reshape(x.shape)
+
+
 def simulate_step(shards: Sequence, x: torch.Tensor, dense: bool) -> torch.Tensor:
     """All shards of one block in ONE process (tests): the collectives become sums / stacks
     in rank order, everything else is exactly what each rank runs."""
@@ -201,4 +280,4 @@ def simulate_step(shards: Sequence, x: torch.Tensor, dense: bool) -> torch.Tenso
 
 
 __all__ = ["split_range", "shard_config", "Comm", "TorchComm", "BlockShard", "ShardedBlock",
-           "simulate_step"]
+           "simulate_step", "token_shard_config", "TokenShardedBlock", "simulate_token_step"]
