@@ -77,6 +77,9 @@ csd_status csd_device_alloc(size_t bytes, void** out);
 csd_status csd_device_free(void* ptr);
 csd_status csd_copy_to_device(void* dst, const void* src, size_t bytes);
 csd_status csd_copy_to_host(void* dst, const void* src, size_t bytes);
+/* Element conversion between fp32 and bf16 device buffers (round to nearest even):
+ * to_bf16 != 0: src fp32 -> dst bf16, else src bf16 -> dst fp32. */
+csd_status csd_cast(csd_ctx* ctx, const void* src, void* dst, int64_t n, int to_bf16, void* stream);
 /* PROD-mode index-set validation on every sparse call (default on; the block
  * runner disables it for its own top-k sets, which are valid by construction). */
 csd_status csd_ctx_set_validation(csd_ctx* ctx, int enabled);

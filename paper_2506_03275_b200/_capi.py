@@ -47,6 +47,7 @@ SIGNATURES = {
     "csd_device_free": (i32, [p]),
     "csd_copy_to_device": (i32, [p, p, C.c_size_t]),
     "csd_copy_to_host": (i32, [p, p, C.c_size_t]),
+    "csd_cast": (i32, [p, fp, fp, i64, C.c_int, p]),
     "csd_mlp_preact": (i32, [p, i32, fp, fp, fp, i64, i64, i64, i64, fp, p]),
     "csd_voxel_permutation": (i32, [i64] * 6 + [p]),
     "csd_voxel_reorder": (i32, [p, fp, fp] + [i64] * 8 + [C.c_int, p]),

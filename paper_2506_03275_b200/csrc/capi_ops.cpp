@@ -489,5 +489,16 @@ csd_status csd_copy_to_host(void* dst, const void* src, size_t bytes) {
     if (bytes) CSD_CU(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "cudaMemcpy d2h");
     return CSD_OK;
 }
+csd_status csd_cast(csd_ctx* ctx, const void* src, void* dst, int64_t n, int to_bf16, void* stream) {
+    auto* c = reinterpret_cast<Ctx*>(ctx);
+    if (!c || (n > 0 && (!src || !dst))) return set_error(CSD_ERR_VALUE, "csd_cast: null argument");
+    if (n < 0) return set_error(CSD_ERR_VALUE, "csd_cast: negative count");
+    if (to_bf16)
+        CSD_CU(prod_cast_f32_bf16(static_cast<const float*>(src), dst, n, S(stream)), "cast");
+    else
+        CSD_CU(prod_cast_bf16_f32(src, static_cast<float*>(dst), n, S(stream)), "cast");
+    c->launches += 1;
+    return CSD_OK;
+}
 
 }  // extern "C"

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cctype>
 #include <iterator>
+#include <memory>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -868,4 +869,239 @@ Tensor model_forward_step(const ToyModel& model, ModelState& state, const Tensor
     return cur;
 }
 
+}  // namespace csd
+
+// ====================================================================== production route
+// include/csd/device.hpp: the same operations on the PROD (bf16 / tcgen05) kernels.
+#include "csd/device.hpp"
+
+namespace csd {
+namespace dev {
+namespace {
+
+// a bf16 device copy of a host fp32 tensor (round to nearest even on the device)
+class Bf16 {
+public:
+    explicit Bf16(const Tensor& t) : d_(2 * static_cast<size_t>(t.numel())) {
+        Dev f(t);
+        ok(csd_cast(ctx(), f.v(), d_.v(), t.numel(), 1, nullptr));
+    }
+    explicit Bf16(int64_t numel) : d_(2 * static_cast<size_t>(numel)) {}
+    void* v() const { return d_.v(); }
+
+private:
+    Dev d_;
+};
+
+Tensor from_bf16(const void* dev_bf16, std::vector<int64_t> shape) {
+    Tensor out(std::move(shape));
+    Dev f(sizeof(float) * static_cast<size_t>(out.numel()));
+    ok(csd_cast(ctx(), dev_bf16, f.v(), out.numel(), 0, nullptr));
+    f.to(out);
+    return out;
+}
+
+}  // namespace
+
+Tensor dense_attention(const Tensor& q, const Tensor& k, const Tensor& v) {  // attention.cpp:59-74
+    check_qkv(q, k, v);
+    Bf16 dq(q), dk(k), dv(v), out(q.numel());
+    ok(csd_dense_attention(ctx(), CSD_MODE_PROD, CSD_LAYOUT_BHNE, dq.v(), dk.v(), dv.v(), q.dim(0),
+                           q.dim(1), q.dim(2), q.dim(3), out.v(), nullptr));
+    sync();
+    return from_bf16(out.v(), q.shape());
+}
+
+ColumnSumAttentionResult column_sum_attention(const Tensor& q, const Tensor& k, const Tensor& v,
+                                              const SoftmaxStats* prev, int64_t chunk) {  // :76-145
+    check_qkv(q, k, v);
+    const int64_t b = q.dim(0), h = q.dim(1), n = q.dim(2), e = q.dim(3);
+    if (chunk < 1 || n % chunk)
+        throw ShapeError("column_sum_attention: sequence length " + std::to_string(n) +
+                         " not divisible by chunk " + std::to_string(chunk));
+    if (prev && (prev->row_max.shape() != std::vector<int64_t>{b, h, n} ||
+                 prev->exp_sum.shape() != std::vector<int64_t>{b, h, n}))
+        throw ShapeError("column_sum_attention: previous stats shape does not match");
+    Bf16 dq(q), dk(k), dv(v), out(q.numel());
+    ColumnSumAttentionResult r;
+    r.stats.row_max = Tensor({b, h, n});
+    r.stats.exp_sum = Tensor({b, h, n});
+    r.column_sums = Tensor({b, h, n / chunk, n});
+    Dev m(sizeof(float) * b * h * n), l(sizeof(float) * b * h * n), cs(sizeof(float) * r.column_sums.numel());
+    std::unique_ptr<Dev> pm, pl;
+    if (prev) {
+        pm = std::make_unique<Dev>(prev->row_max);
+        pl = std::make_unique<Dev>(prev->exp_sum);
+    }
+    ok(csd_column_sum_attention(ctx(), CSD_MODE_PROD, CSD_LAYOUT_BHNE, dq.v(), dk.v(), dv.v(),
+                                pm ? pm->f() : nullptr, pl ? pl->f() : nullptr, b, h, n, e, chunk,
+                                out.v(), m.f(), l.f(), cs.f(), nullptr));
+    sync();
+    r.output = from_bf16(out.v(), q.shape());
+    m.to(r.stats.row_max);
+    l.to(r.stats.exp_sum);
+    cs.to(r.column_sums);
+    return r;
+}
+
+Tensor sparse_delta_attention(const Tensor& q, const Tensor& k, const Tensor& v,
+                              const SparseIndexSet& idx, const Tensor& base, float scale) {  // :147-194
+    check_qkv(q, k, v);
+    check_index_set(idx, q);
+    if (base.shape() != q.shape())
+        throw ShapeError("sparse_delta_attention: base " + shape_str(base.shape()) +
+                         " does not match q " + shape_str(q.shape()));
+    Bf16 dq(q), dk(k), dv(v), db(base), out(q.numel());
+    Dev di(idx.indices), dc(idx.counts);
+    ok(csd_sparse_delta_attention(ctx(), CSD_MODE_PROD, CSD_LAYOUT_BHNE, dq.v(), dk.v(), dv.v(),
+                                  di.i(), dc.i(), idx.k_max, idx.chunk_size, db.v(), scale, q.dim(0),
+                                  q.dim(1), q.dim(2), q.dim(3), out.v(), nullptr));
+    sync();  // surfaces the on-device index validation as IndexError / ValueError
+    return from_bf16(out.v(), q.shape());
+}
+
+MlpDenseResult dense_mlp(const Tensor& x, const MlpWeights& w, int64_t chunk) {  // mlp.cpp:49-81
+    check_x(x, w);
+    const int64_t b = x.dim(0), n = x.dim(1), d = x.dim(2), f = w.w1.dim(0);
+    if (chunk < 1 || n % chunk)
+        throw ShapeError("dense_mlp: sequence length " + std::to_string(n) + " not divisible by chunk " +
+                         std::to_string(chunk));
+    Bf16 dx(x), dw1(w.w1), dw2(w.w2), act(b * n * f);
+    Dev db1(w.b1), db2(w.b2), out(sizeof(float) * b * n * d), aref(sizeof(float) * b * n * f);
+    ok(csd_dense_mlp(ctx(), CSD_MODE_PROD, dx.v(), dw1.v(), db1.f(), dw2.v(), db2.f(), b, n, d, f,
+                     chunk, out.f(), act.v(), nullptr));
+    ok(csd_mlp_act_cache_to_ref(ctx(), CSD_MODE_PROD, act.v(), b, n, f, chunk, aref.f(), nullptr));
+    sync();
+    MlpDenseResult r;
+    r.output = Tensor({b, n, d});
+    r.act = Tensor({b, n, f});
+    out.to(r.output);
+    aref.to(r.act);
+    return r;  // preact stays empty: the fused GEMM never materialises x W1^T + b1
+}
+
+Tensor mlp_tile_means(const Tensor& x, const Tensor& w1, int64_t chunk) {  // mlp.cpp:83-96
+    if (x.rank() != 3 || w1.rank() != 2 || w1.dim(1) != x.dim(2))
+        throw ShapeError("mlp_tile_means: x " + shape_str(x.shape()) + " and w1 " + shape_str(w1.shape()) +
+                         " disagree");
+    const int64_t b = x.dim(0), n = x.dim(1), d = x.dim(2), f = w1.dim(0);
+    if (chunk < 1 || n % chunk)
+        throw ShapeError("mlp_tile_means: sequence length not divisible by chunk");
+    Bf16 dx(x), dw1(w1);
+    Tensor out({b, n / chunk, f});
+    Dev dout(sizeof(float) * out.numel());
+    ok(csd_mlp_tile_means(ctx(), CSD_MODE_PROD, dx.v(), dw1.v(), b, n, d, f, chunk, dout.f(), nullptr));
+    sync();
+    dout.to(out);
+    return out;
+}
+
+SparseIndexSet mlp_change_indices(const Tensor& x, const Tensor& w1, const Tensor& tile_means,
+                                  int64_t k, int64_t chunk) {  // mlp.cpp:98-118
+    if (x.rank() != 3 || w1.rank() != 2 || w1.dim(1) != x.dim(2))
+        throw ShapeError("mlp_change_indices: x " + shape_str(x.shape()) + " and w1 " +
+                         shape_str(w1.shape()) + " disagree");
+    const int64_t b = x.dim(0), n = x.dim(1), d = x.dim(2), f = w1.dim(0);
+    if (chunk < 1 || n % chunk) throw ShapeError("mlp_change_indices: sequence length not divisible by chunk");
+    if (tile_means.shape() != std::vector<int64_t>{b, n / chunk, f})
+        throw ShapeError("mlp_change_indices: tile means " + shape_str(tile_means.shape()) +
+                         " do not match the input");
+    if (k < 0 || k > f) throw ValueError("mlp_change_indices: k " + std::to_string(k) + " outside [0, F]");
+    Bf16 dx(x), dw1(w1);
+    Dev dtm(tile_means);
+    SparseIndexSet s = SparseIndexSet::empty(b, 1, n / chunk, chunk, k, f);
+    Dev di(sizeof(int32_t) * s.indices.size()), dc(sizeof(int32_t) * s.counts.size());
+    ok(csd_mlp_change_indices(ctx(), CSD_MODE_PROD, dx.v(), dw1.v(), dtm.f(), b, n, d, f, k, chunk,
+                              di.i(), dc.i(), nullptr));
+    sync();
+    di.to(s.indices);
+    dc.to(s.counts);
+    return s;
+}
+
+// ---------------------------------------------------------------- DeviceModel
+DeviceModel::DeviceModel(const ToyModel& model, const SparsityConfig& sparsity)
+    : cfg_(model.cfg), sparsity_(sparsity) {
+    cfg_.validate();
+    csd_block_config c{};
+    c.batch = cfg_.batch;
+    c.seq = cfg_.seq_len();
+    c.dim = cfg_.model_dim;
+    c.heads = cfg_.heads;
+    c.head_dim = cfg_.head_dim;
+    c.hidden = cfg_.mlp_hidden;
+    c.chunk = cfg_.chunk;
+    c.attn_k = sparsity.attn_k;
+    c.mlp_k = sparsity.mlp_k;
+    for (const auto& lw : model.layers) {
+        csd_block* blk = nullptr;
+        const csd_status s =
+            csd_block_create(ctx(), CSD_MODE_PROD, &c, lw.wq.data(), lw.wk.data(), lw.wv.data(),
+                             lw.wo.data(), lw.mlp.w1.data(), lw.mlp.b1.data(), lw.mlp.w2.data(),
+                             lw.mlp.b2.data(), &blk);
+        if (s != CSD_OK) {
+            for (void* b : blocks_) csd_block_destroy(static_cast<csd_block*>(b));
+            blocks_.clear();
+            rethrow(s);
+        }
+        blocks_.push_back(blk);
+    }
+    const size_t elems = static_cast<size_t>(c.batch * c.seq * c.dim);
+    ok(csd_device_alloc(2 * elems, &buf_[0]));
+    ok(csd_device_alloc(2 * elems, &buf_[1]));
+    ok(csd_device_alloc(4 * elems, &io_));
+}
+
+DeviceModel::~DeviceModel() {
+    for (void* b : blocks_) csd_block_destroy(static_cast<csd_block*>(b));
+    csd_device_free(buf_[0]);
+    csd_device_free(buf_[1]);
+    csd_device_free(io_);
+}
+
+void DeviceModel::reset() {
+    for (void* b : blocks_) ok(csd_block_reset(static_cast<csd_block*>(b)));
+}
+
+void DeviceModel::forward_step_device(const void* x_bf16, void* y_bf16, bool dense_step, void* stream) {
+    // layer l reads the previous layer's output; the last one writes y
+    const void* in = x_bf16;
+    for (size_t l = 0; l < blocks_.size(); ++l) {
+        void* out = l + 1 == blocks_.size() ? y_bf16 : buf_[l & 1];
+        ok(csd_block_step(static_cast<csd_block*>(blocks_[l]), in, out, dense_step ? 1 : 0, nullptr,
+                          nullptr, 0, stream));
+        in = out;
+    }
+    if (blocks_.empty()) {  // a zero-layer model is the identity (model.cpp:184-186)
+        const size_t bytes = 2 * static_cast<size_t>(cfg_.batch * cfg_.seq_len() * cfg_.model_dim);
+        std::vector<char> tmp(bytes);
+        ok(csd_copy_to_host(tmp.data(), x_bf16, bytes));
+        ok(csd_copy_to_device(y_bf16, tmp.data(), bytes));
+    }
+}
+
+Tensor DeviceModel::forward_step(const Tensor& x, bool dense_step, const SparseIndexSet* static_attn) {
+    const int64_t b = cfg_.batch, n = cfg_.seq_len(), d = cfg_.model_dim;
+    if (x.shape() != std::vector<int64_t>{b, n, d})
+        throw ShapeError("model_forward_step: input " + shape_str(x.shape()) + " does not match the model");
+    ok(csd_copy_to_device(io_, x.data(), sizeof(float) * x.numel()));
+    ok(csd_cast(ctx(), io_, buf_[0], x.numel(), 1, nullptr));
+    std::unique_ptr<Dev> si, sc;
+    if (static_attn) {
+        si = std::make_unique<Dev>(static_attn->indices);
+        sc = std::make_unique<Dev>(static_attn->counts);
+    }
+    // ping-pong through the two bf16 buffers (buf_[0] holds x)
+    int cur = 0;
+    for (void* bp : blocks_) {
+        ok(csd_block_step(static_cast<csd_block*>(bp), buf_[cur], buf_[1 - cur], dense_step ? 1 : 0,
+                          si ? si->i() : nullptr, sc ? sc->i() : nullptr,
+                          static_attn ? static_attn->k_max : 0, nullptr));
+        cur = 1 - cur;
+    }
+    sync();
+    return from_bf16(buf_[cur], x.shape());
+}
+
+}  // namespace dev
 }  // namespace csd
