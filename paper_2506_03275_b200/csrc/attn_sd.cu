@@ -378,7 +378,11 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 l_run += part.x + part.y;
                 if (kCs) {
                     // W[slot][row] = w, W[1 - slot][row] = 0 (bf16, K-major 128B-swizzled rows)
-                    const float w = row_ok ? ex2_approx(m_run - mpl) * inv_lp : 0.f;
+                    // stale stats far below the fresh logits: the reference's fp32 exp overflows
+                    // to +inf for the keys past ~88 nats (attention.cpp:135); a finite cap keeps
+                    // those products overflowing (p w -> +inf in the MMA) without turning the
+                    // masked p = 0 entries into inf * 0 = NaN
+                    const float w = row_ok ? fminf(ex2_approx(m_run - mpl) * inv_lp, 3.0e38f) : 0.f;
                     const __nv_bfloat16 wb = __float2bfloat16_rn(w), zb = __float2bfloat16_rn(0.f);
                     uint8_t* ws = sw + (row >> 6) * 2048;
                     const int kc = (row & 63) >> 3, ke = row & 7;
