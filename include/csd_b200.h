@@ -88,6 +88,10 @@ csd_status csd_ctx_set_validation(csd_ctx* ctx, int enabled);
  * lowest-index ties, each in index order (what the PROD block path uses: its consumers are
  * order-invariant; lets few long rows run as a cluster of CTAs per row). */
 csd_status csd_ctx_set_sorted_topk(csd_ctx* ctx, int sorted);
+/* Longest-first (LPT) order of the (b, h, chunk) work items of PROD sparse attention over a
+ * ragged index set (default on; one small ordering kernel per call).  Results do not depend
+ * on it. */
+csd_status csd_ctx_set_lpt(csd_ctx* ctx, int enabled);
 /* Number of kernels this context launched since creation (instrumentation). */
 int64_t csd_ctx_launch_count(const csd_ctx* ctx);
 

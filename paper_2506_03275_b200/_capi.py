@@ -43,6 +43,7 @@ SIGNATURES = {
     "csd_ctx_launch_count": (i64, [p]),
     "csd_ctx_set_validation": (i32, [p, C.c_int]),
     "csd_ctx_set_sorted_topk": (i32, [p, C.c_int]),
+    "csd_ctx_set_lpt": (i32, [p, C.c_int]),
     "csd_device_alloc": (i32, [C.c_size_t, C.POINTER(p)]),
     "csd_device_free": (i32, [p]),
     "csd_copy_to_device": (i32, [p, p, C.c_size_t]),

@@ -82,6 +82,7 @@ struct PPParams {
     const __nv_bfloat16* vp;
     float qk_scale_log2;
     int warm;  // dead softmax warps warm the instruction cache (see the softmax branch)
+    const int32_t* order;  // work position -> item (longest first), or null (identity)
     uint64_t* span;  // debug per-CTA [start, end] globaltimer (null: off)
     uint64_t* trace;  // debug timeline (null: off): kPPTraceCtas x 1024 clock64 stamps
 };
@@ -163,7 +164,10 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         mbar_init(bar_xc, (uint32_t)(lw0 + lw1));
         fence_barrier_init();
     }
-    auto count_of = [&](int it) -> int { return dense ? p.n : p.counts[it]; };
+    // work positions -> items: longest-first order for ragged index sets (p.order, LPT), or
+    // the identity; every role walks POSITIONS pos = blockIdx.x + i * gridDim.x
+    auto item_at = [&](int pos) -> int { return p.order != nullptr ? p.order[pos] : pos; };
+    auto count_of = [&](int pos) -> int { return dense ? p.n : p.counts[item_at(pos)]; };
     // next live (count > 0) item of this CTA at or after `from`
     auto next_live = [&](int from, int& cnt_out) -> int {
         int x = from;
@@ -174,7 +178,8 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         }
         return x;
     };
-    auto item_rows = [&](int it, int& row_base, int& col0) {
+    auto item_rows = [&](int pos, int& row_base, int& col0) {
+        const int it = item_at(pos);
         const int bh = it / p.chunks;
         row_base = p.layout == CSD_LAYOUT_BHNE ? bh * p.n : (bh / p.heads) * p.n;
         col0 = p.layout == CSD_LAYOUT_BHNE ? 0 : (bh % p.heads) * E;
@@ -189,7 +194,7 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     const int cp_thread = warp < 4 ? (warp - 2) * 32 + lane : 64 + (warp - 12) * 32 + lane;
     auto load_ids = [&](int it, int cnt, int j, int32_t (&id)[kCpRows]) {
         const int r0 = cp_thread / (E / 8);
-        const int32_t* ids = p.idx + (int64_t)(it < items ? it : 0) * p.k_max;
+        const int32_t* ids = p.idx + (int64_t)(it < items ? item_at(it) : 0) * p.k_max;
 #pragma unroll
         for (int i = 0; i < kCpRows; ++i) {
             const int r = j * 128 + r0 + kRowStep * i;
@@ -249,7 +254,7 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 for (int it = next_live(blockIdx.x, cnt); it < items; it = next_live(it + gridDim.x, cnt)) {
                     int r0, col0;
                     item_rows(it, r0, col0);
-                    const int kr0 = r0 - (it % p.chunks) * p.chunk;  // the sequence's row 0
+                    const int kr0 = r0 - (item_at(it) % p.chunks) * p.chunk;  // the sequence's row 0
                     const int nblk = (cnt + 127) / 128;
                     for (int j = 0; j < nblk; ++j, ++gb) {
                         const int s = gb & 1;
@@ -444,7 +449,7 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
 #pragma unroll
             for (int i = 0; i < kCpRows; ++i) id[i] = cp_id[i];
             for (uint32_t g = 0; it < items; ++g) {
-                const int bh = it / p.chunks;
+                const int bh = item_at(it) / p.chunks;
                 const int64_t o0 = pp_tok_off(p.layout, bh / p.heads, bh % p.heads, 0, p.heads, p.n, E) + c16 * 8;
                 const __nv_bfloat16* kb = p.kp + o0;
                 const __nv_bfloat16* vb = p.vp + o0;
@@ -521,7 +526,8 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             for (int it = blockIdx.x; it < items; it += gridDim.x) {
                 const int cnt = cnt_nx;  // loaded one item ahead
                 if (it + (int)gridDim.x < items) cnt_nx = count_of(it + gridDim.x);
-                const int c = it % p.chunks, bh = it / p.chunks;
+                const int item = item_at(it);
+                const int c = item % p.chunks, bh = item / p.chunks;
                 const int b = bh / p.heads, h = bh % p.heads;
                 const int64_t tok = (int64_t)c * p.chunk + crow;
                 if (cnt == 0) {  // pass base through (attention.cpp:169)
@@ -761,6 +767,7 @@ cudaError_t launch_pp(const AttnTcArgs& a, cudaStream_t s) {
     p.vp = static_cast<const __nv_bfloat16*>(a.v);
     p.qk_scale_log2 = kLog2e / std::sqrt((float)E);
     p.span = h_pp_span;
+    p.order = a.order;
     {
         static const int warm = [] {
             const char* e = std::getenv("CSD_PP_WARM");
@@ -808,6 +815,53 @@ cudaError_t launch_pp(const AttnTcArgs& a, cudaStream_t s) {
 }
 
 }  // namespace
+
+namespace {
+// counting sort of the items by descending key-block count (ties in item order)
+__global__ void __launch_bounds__(1024) k_lpt_order(const int32_t* __restrict__ counts, int items,
+                                                    int block_keys, int32_t* __restrict__ order) {
+    constexpr int kBins = 512;
+    __shared__ int hist[kBins], base[kBins];
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    auto bin_of = [&](int it) {
+        const int nb = (max(counts[it], 0) + block_keys - 1) / block_keys;
+        return kBins - 1 - min(nb, kBins - 1);  // more blocks -> earlier bin
+    };
+    for (int it = threadIdx.x; it - (int)(threadIdx.x & 31) < items; it += blockDim.x) {
+        const int b = it < items ? bin_of(it) : -1;  // warp-aggregated counts
+        const unsigned m = __match_any_sync(0xffffffffu, b);
+        if ((int)(threadIdx.x & 31) == __ffs(m) - 1 && b >= 0) atomicAdd(&hist[b], __popc(m));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int b = 0; b < kBins; ++b) {
+            base[b] = run;
+            run += hist[b];
+        }
+    }
+    __syncthreads();
+    // warp-aggregated slots (order within a bin is arbitrary: each item's result does not
+    // depend on which CTA runs it)
+    for (int it = threadIdx.x; it - (int)(threadIdx.x & 31) < items; it += blockDim.x) {
+        const int b = it < items ? bin_of(it) : -1;
+        const unsigned m = __match_any_sync(0xffffffffu, b);
+        const int leader = __ffs(m) - 1;
+        const int rank = __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
+        int pos = 0;
+        if ((int)(threadIdx.x & 31) == leader && b >= 0) pos = atomicAdd(&base[b], __popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, leader);
+        if (b >= 0) order[pos + rank] = it;
+    }
+}
+}  // namespace
+
+cudaError_t lpt_order(const int32_t* counts, int64_t items, int64_t block_keys, int32_t* order,
+                      cudaStream_t s) {
+    k_lpt_order<<<1, 1024, 0, s>>>(counts, (int)items, (int)block_keys, order);
+    return cudaGetLastError();
+}
 
 bool attn_pp_supported(const AttnTcArgs& a) {
     static const bool off = [] {

@@ -343,6 +343,14 @@ static csd_status attn_core(csd_block* blk, const void* x_in, int dense, const i
         ~ValidateGuard() { c->validate_prod = old; }
     } vguard{blk->ctx, blk->ctx->validate_prod};
     blk->ctx->validate_prod = false;
+    // the block's own top-k sets have count k in every chunk: nothing for LPT to balance;
+    // a caller's static pattern is ragged
+    struct LptGuard {
+        Ctx* c;
+        bool old;
+        ~LptGuard() { c->lpt = old; }
+    } lguard{blk->ctx, blk->ctx->lpt};
+    blk->ctx->lpt = static_idx != nullptr;
     if (dense) {
         // PROD reads the stale stats and writes the fresh ones row-by-row in the
         // same thread, so one buffer suffices (and the step stays graph-capturable);

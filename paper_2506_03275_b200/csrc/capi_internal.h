@@ -27,6 +27,7 @@ enum WsSlot {
     kWsIdx,
     kWsCounts,
     kWsR2,
+    kWsOrder,
     kWsCount
 };
 
@@ -46,6 +47,9 @@ struct Ctx {
     // sparse-delta MLP) are order-invariant, so the same exact index SET in index order
     // skips the per-row sort.
     bool sorted_topk = true;
+    // sparse attention over ragged index sets: items ordered longest-first (lpt_order).  The
+    // block path clears it for its own top-k sets (every count == k: nothing to balance).
+    bool lpt = true;
 
     // Workspace slot of at least `bytes`; `s` (the calling op's stream) lets a growth during
     // stream capture fail loudly instead of allocating inside the capture.

@@ -128,6 +128,12 @@ csd_status csd_ctx_set_validation(csd_ctx* ctx, int enabled) {
     return CSD_OK;
 }
 
+csd_status csd_ctx_set_lpt(csd_ctx* ctx, int enabled) {
+    if (!ctx) return set_error(CSD_ERR_VALUE, "null context");
+    reinterpret_cast<Ctx*>(ctx)->lpt = enabled != 0;
+    return CSD_OK;
+}
+
 csd_status csd_ctx_set_sorted_topk(csd_ctx* ctx, int sorted) {
     if (!ctx) return set_error(CSD_ERR_VALUE, "null context");
     reinterpret_cast<Ctx*>(ctx)->sorted_topk = sorted != 0;
@@ -250,6 +256,14 @@ csd_status csd_sparse_delta_attention(csd_ctx* ctx, csd_mode mode, csd_layout la
         a.q = q; a.k = k; a.v = v; a.idx = idx; a.counts = counts; a.k_max = k_max;
         a.base = base; a.scale = scale; a.out = out; a.layout = layout;
         a.batch = batch; a.heads = heads; a.n = n; a.e = e; a.chunk = chunk;
+        if (c->lpt && attn_pp_supported(a) && k_max > 128) {
+            // ragged counts: longest items first over the persistent CTAs
+            auto* order = static_cast<int32_t*>(c->ws(csd::kWsOrder, sizeof(int32_t) * rows, s));
+            CSD_TRY(need_ws(order));
+            CSD_CU(lpt_order(counts, rows, 128, order, s), "lpt_order");
+            c->launches += 1;
+            a.order = order;
+        }
         return prod_attn(c, a, s);
     }
     CSD_TRY(sync_validate(c, idx, counts, rows, k_max, n, s));

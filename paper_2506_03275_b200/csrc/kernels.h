@@ -97,7 +97,14 @@ struct AttnTcArgs {
     // column sums are per cs_chunk rows, accumulated atomically into a zeroed colsum);
     // 0 = the item rows
     int64_t cs_chunk;
+    // sparse: work position -> item, longest first (lpt_order), or null (identity order)
+    const int32_t* order;
 };
+// Longest-processing-time order of the (b, h, chunk) items of a ragged index set: items
+// sorted by descending key-block count (counting sort, one CTA); persistent CTAs then take
+// positions b, b + grid, ... (attn_pp.cu).
+cudaError_t lpt_order(const int32_t* counts, int64_t items, int64_t block_keys, int32_t* order,
+                      cudaStream_t s);
 // Returns cudaErrorNotSupported for shapes outside the envelope.
 cudaError_t attn_tc(const AttnTcArgs& a, cudaStream_t s);
 bool attn_tc_supported(int64_t e, int64_t chunk);
