@@ -272,15 +272,18 @@ csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int den
             CSD_TRY(csd::gemm_bf16(blk->ctx, blk->attn, blk->wo, false, blk->x_mid, false, B * N, D,
                                    Dl, 1.0f, s));
         }
-        // ---- MLP branch; x2 = x1 + M is fused into the last MLP kernel's epilogue
-        if (dense) {
+        // ---- MLP branch; x2 = x1 + M is fused into the last MLP kernel's epilogue.  With
+        // mlp_k >= F every neuron is recomputed on a sparse step (mlp.cpp:120-182 with the full
+        // index set), which is the dense MLP with the cache refreshed (WAN-style configs)
+        if (dense || mk >= Fl) {
             CSD_TRY(csd::prod_dense_mlp(blk->ctx, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B,
                                         N, D, Fl, c.chunk, blk->mout, blk->act, blk->x_mid, x_out,
                                         s));
-            CSD_TRY(csd_mlp_tile_means(ctx, md, blk->x_mid, blk->w1, B, N, D, Fl, c.chunk,
-                                       blk->tmeans, stream));
+            if (dense)  // the selection signal (unused when every neuron is recomputed)
+                CSD_TRY(csd_mlp_tile_means(ctx, md, blk->x_mid, blk->w1, B, N, D, Fl, c.chunk,
+                                           blk->tmeans, stream));
             blk->mlp_init = true;
-            blk->mlp_age = 0;
+            blk->mlp_age = dense ? 0 : blk->mlp_age + 1;
         } else {
             CSD_TRY(csd_mlp_change_indices(ctx, md, blk->x_mid, blk->w1, blk->tmeans, B, N, D, Fl,
                                            mk, c.chunk, blk->midx, blk->mcnt, stream));
