@@ -447,9 +447,14 @@ def attention_kernel_bench(ops, torch, cfg, n, attn_k, reps, dense_ms=None, flus
         torch.cuda.synchronize()
         return statistics.median(a.elapsed_time(b) for a, b in evs[3:])
 
-    ops.context().set_validation(False)  # the index set comes from top-k: valid by construction
+    # the index set comes from top-k: valid by construction and uniform (count k in every
+    # chunk), so -- as in the block step -- no validation pass and no LPT ordering pass
+    ctx = ops.context()
+    ctx.set_validation(False)
+    ctx.lib.csd_ctx_set_lpt(ctx.h, 0)
     t_sparse = timed(lambda: ops.sparse_delta_attention(q, k, v, idx, base, 1.0, layout=1, out=out))
-    ops.context().set_validation(True)
+    ctx.lib.csd_ctx_set_lpt(ctx.h, 1)
+    ctx.set_validation(True)
     t_dense = dense_ms if dense_ms is not None else timed(lambda: ops.dense_attention(q, k, v, layout=1))
     # the dense STEP's pass: dense attention + stale-stat chunk column sums (attention.cpp:76-145)
     stats = r.stats

@@ -81,7 +81,7 @@ struct PPParams {
     const __nv_bfloat16* kp;
     const __nv_bfloat16* vp;
     float qk_scale_log2;
-    int warm;  // dead softmax warps warm the instruction cache (see the softmax branch)
+    int warm;  // dead softmax warps run the first item as an icache warm-up (softmax branch)
     const int32_t* order;  // work position -> item (longest first), or null (identity)
     uint64_t* span;  // debug per-CTA [start, end] globaltimer (null: off)
     uint64_t* trace;  // debug timeline (null: off): kPPTraceCtas x 1024 clock64 stamps
@@ -166,7 +166,8 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     }
     // work positions -> items: longest-first order for ragged index sets (p.order, LPT), or
     // the identity; every role walks POSITIONS pos = blockIdx.x + i * gridDim.x
-    auto item_at = [&](int pos) -> int { return p.order != nullptr ? p.order[pos] : pos; };
+    const int32_t* order = (p.order != nullptr && p.order[items] == 0) ? p.order : nullptr;
+    auto item_at = [&](int pos) -> int { return order != nullptr ? order[pos] : pos; };
     auto count_of = [&](int pos) -> int { return dense ? p.n : p.counts[item_at(pos)]; };
     // next live (count > 0) item of this CTA at or after `from`
     auto next_live = [&](int from, int& cnt_out) -> int {
@@ -817,43 +818,64 @@ cudaError_t launch_pp(const AttnTcArgs& a, cudaStream_t s) {
 }  // namespace
 
 namespace {
-// counting sort of the items by descending key-block count (ties in item order)
+// Stable counting sort of the items by descending key-block count (ties keep item order, so
+// uniform counts give the identity -- the strided order whose concurrent items share heads
+// in L2).  order[items] = 1 flags the identity, letting the attention kernel skip the
+// indirection.  Tiles of 1024 items: per-warp bin counts, a cross-warp scan per bin, ranks
+// within a warp by __match_any_sync.
+constexpr int kLptBins = 64;  // key-block counts >= 63 share the first bin
 __global__ void __launch_bounds__(1024) k_lpt_order(const int32_t* __restrict__ counts, int items,
                                                     int block_keys, int32_t* __restrict__ order) {
-    constexpr int kBins = 512;
-    __shared__ int hist[kBins], base[kBins];
-    for (int i = threadIdx.x; i < kBins; i += blockDim.x) hist[i] = 0;
+    __shared__ int hist[kLptBins], base[kLptBins];
+    __shared__ int wcnt[32][kLptBins];
+    __shared__ int not_ident;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kLptBins; i += blockDim.x) hist[i] = 0;
+    if (threadIdx.x == 0) not_ident = 0;
     __syncthreads();
     auto bin_of = [&](int it) {
         const int nb = (max(counts[it], 0) + block_keys - 1) / block_keys;
-        return kBins - 1 - min(nb, kBins - 1);  // more blocks -> earlier bin
+        return kLptBins - 1 - min(nb, kLptBins - 1);  // more blocks -> earlier bin
     };
-    for (int it = threadIdx.x; it - (int)(threadIdx.x & 31) < items; it += blockDim.x) {
-        const int b = it < items ? bin_of(it) : -1;  // warp-aggregated counts
+    for (int it = threadIdx.x; it - lane < items; it += blockDim.x) {
+        const int b = it < items ? bin_of(it) : -1;
         const unsigned m = __match_any_sync(0xffffffffu, b);
-        if ((int)(threadIdx.x & 31) == __ffs(m) - 1 && b >= 0) atomicAdd(&hist[b], __popc(m));
+        if (lane == __ffs(m) - 1 && b >= 0) atomicAdd(&hist[b], __popc(m));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        int run = 0;
-        for (int b = 0; b < kBins; ++b) {
+        int run = 0, used = 0;
+        for (int b = 0; b < kLptBins; ++b) {
             base[b] = run;
             run += hist[b];
+            used += hist[b] > 0;
         }
+        if (used > 1) not_ident = 1;  // one bin only: the stable order is the identity
     }
     __syncthreads();
-    // warp-aggregated slots (order within a bin is arbitrary: each item's result does not
-    // depend on which CTA runs it)
-    for (int it = threadIdx.x; it - (int)(threadIdx.x & 31) < items; it += blockDim.x) {
+    for (int t0 = 0; t0 < items; t0 += blockDim.x) {
+        const int it = t0 + threadIdx.x;
         const int b = it < items ? bin_of(it) : -1;
         const unsigned m = __match_any_sync(0xffffffffu, b);
-        const int leader = __ffs(m) - 1;
-        const int rank = __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
-        int pos = 0;
-        if ((int)(threadIdx.x & 31) == leader && b >= 0) pos = atomicAdd(&base[b], __popc(m));
-        pos = __shfl_sync(0xffffffffu, pos, leader);
-        if (b >= 0) order[pos + rank] = it;
+        const int rank = __popc(m & ((1u << lane) - 1u));
+        for (int i = threadIdx.x; i < 32 * kLptBins; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+        __syncthreads();
+        if (b >= 0 && lane == __ffs(m) - 1) wcnt[warp][b] = __popc(m);
+        __syncthreads();
+        if (threadIdx.x < kLptBins) {  // exclusive scan over warps, per bin
+            int run = base[threadIdx.x];
+            for (int w = 0; w < 32; ++w) {
+                const int c = wcnt[w][threadIdx.x];
+                wcnt[w][threadIdx.x] = run;
+                run += c;
+            }
+            base[threadIdx.x] = run;
+        }
+        __syncthreads();
+        if (b >= 0) order[wcnt[warp][b] + rank] = it;
+        __syncthreads();
     }
+    if (threadIdx.x == 0) order[items] = not_ident ? 0 : 1;
 }
 }  // namespace
 

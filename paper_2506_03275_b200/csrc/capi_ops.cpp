@@ -258,7 +258,7 @@ csd_status csd_sparse_delta_attention(csd_ctx* ctx, csd_mode mode, csd_layout la
         a.batch = batch; a.heads = heads; a.n = n; a.e = e; a.chunk = chunk;
         if (c->lpt && attn_pp_supported(a) && k_max > 128) {
             // ragged counts: longest items first over the persistent CTAs
-            auto* order = static_cast<int32_t*>(c->ws(csd::kWsOrder, sizeof(int32_t) * rows, s));
+            auto* order = static_cast<int32_t*>(c->ws(csd::kWsOrder, sizeof(int32_t) * (rows + 1), s));
             CSD_TRY(need_ws(order));
             CSD_CU(lpt_order(counts, rows, 128, order, s), "lpt_order");
             c->launches += 1;

@@ -101,8 +101,9 @@ struct AttnTcArgs {
     const int32_t* order;
 };
 // Longest-processing-time order of the (b, h, chunk) items of a ragged index set: items
-// sorted by descending key-block count (counting sort, one CTA); persistent CTAs then take
-// positions b, b + grid, ... (attn_pp.cu).
+// sorted stably by descending key-block count (counting sort, one CTA) into order[0, items),
+// order[items] = 1 when that is the identity; persistent CTAs then take positions b,
+// b + grid, ... (attn_pp.cu).
 cudaError_t lpt_order(const int32_t* counts, int64_t items, int64_t block_keys, int32_t* order,
                       cudaStream_t s);
 // Returns cudaErrorNotSupported for shapes outside the envelope.

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--sparsity", type=float, default=0.93)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between reps")
+    ap.add_argument("--no-lpt", action="store_true", help="identity item order")
     args = ap.parse_args()
     cfg = dict(bench.FLUX)
     n = cfg["grid"][1] * cfg["grid"][2]
@@ -47,6 +48,8 @@ def main():
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
         return
+    if args.no_lpt:
+        ops.context().lib.csd_ctx_set_lpt(ops.context().h, 0)
     res = bench.attention_kernel_bench(ops, torch, cfg, n, ak, args.reps, flush_l2=not args.no_flush)
     print(json.dumps(res))
 

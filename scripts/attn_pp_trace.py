@@ -28,6 +28,11 @@ def main():
     ap.add_argument("--ctas", type=int, default=2)
     ap.add_argument("--dense", action="store_true")
     ap.add_argument("--blocks", type=int, default=40)
+    ap.add_argument("--back-to-back", action="store_true",
+                    help="trace a launch issued right after an identical one (warm caches)")
+    ap.add_argument("--flush", action="store_true", help="write 256 MB before the traced launch")
+    ap.add_argument("--in-step", action="store_true",
+                    help="trace the attention launch inside a FLUX block sparse step")
     args = ap.parse_args()
     cfg = dict(bench.FLUX)
     n = cfg["grid"][1] * cfg["grid"][2]
@@ -50,6 +55,24 @@ def main():
     buf = torch.zeros(8 * 2048, dtype=torch.int64, device="cuda")
     torch.cuda.synchronize()
     fn(buf.data_ptr())
+    if args.flush:
+        torch.empty(64 * 1024 * 1024, device="cuda").fill_(1.0)
+    if args.back_to_back:
+        fn(None)
+        run()  # untraced, immediately before
+        fn(buf.data_ptr())
+    if args.in_step:
+        fn(None)
+        bc = ops.BlockConfig(batch=1, seq=n, dim=cfg["dim"], heads=h, head_dim=e, hidden=cfg["hidden"],
+                             chunk=c, attn_k=ak, mlp_k=bench.k_of(cfg["hidden"], args.sparsity))
+        blk = ops.Block(bc, bench.make_weights(cfg), production=True)
+        xb = torch.randn((1, n, cfg["dim"]), device="cuda", generator=g).to(torch.bfloat16)
+        blk.step(xb, True)
+        blk.step(xb, False)
+        blk.step(xb, False)
+        torch.cuda.synchronize()
+        fn(buf.data_ptr())
+        run = lambda: blk.step(xb, False)  # noqa: E731
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     run()
