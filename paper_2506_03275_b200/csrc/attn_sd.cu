@@ -22,9 +22,9 @@
 // (a 128-row tile meets at most two chunks of 64..256 rows and a chunk at most two tiles),
 // so the sums are order-independent and exact in fp32 accumulation.
 //
-// Roles (12 warps): warp 0 lane 0 Q loader, lane 1 K/V TMA loader; warp 1 MMA issuer;
-// warps 4-7 softmax + epilogue (one thread per query row, all 128 columns of a block);
-// warps 8-11 column-sum readers.
+// Roles (16 warps): warp 0 lane 0 Q loader, lane 1 K/V TMA loader; warp 1 MMA issuer;
+// warps 4-11 softmax + epilogue (two warps per query-row quadrant, 64 key columns each);
+// warps 12-15 column-sum readers.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -60,14 +60,15 @@ struct SDLayout {
     static constexpr uint32_t kQ = kHalves * kStrip;
     static constexpr uint32_t kP = 2 * kStrip;         // P copy: 128 rows x 128 keys bf16
     static constexpr uint32_t kW = 2 * 16 * 128;       // W: 16 rows x 128 K, two K strips
-    static constexpr uint32_t kThreads = 384;
+    static constexpr uint32_t kThreads = 512;
+    static constexpr uint32_t kXch = 2 * 128 * 2 * 4 + 128 * 2 * 4;  // row-half max / sum exchange
     static constexpr uint32_t kOcol = 256;
     static constexpr uint32_t kCscol = 256 + E;
     static constexpr uint32_t kMaxSmem = 227 * 1024;
 };
 
 struct SDParams {
-    uint32_t off_k, off_v, off_p, off_w, off_bar;
+    uint32_t off_k, off_v, off_p, off_w, off_x, off_bar;
     int layout, heads, n, tiles, items;  // tiles: 128-row tiles per (b, h)
     __nv_bfloat16* out;
     float* row_max;
@@ -116,6 +117,8 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     uint8_t* const sv = smem + p.off_v;
     uint8_t* const sp = smem + p.off_p;
     uint8_t* const sw = smem + p.off_w;
+    float* const xch = reinterpret_cast<float*>(smem + p.off_x);       // [2][128][2] block maxima
+    float* const lxch = xch + 2 * 128 * 2;                              // [128][2] row sums
     if (threadIdx.x == 0) {
         if ((raw_u32 & 1023u) != 0) __trap();
         mbar_init(bar_q, 1);
@@ -128,7 +131,7 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             mbar_init(bar_s + i, 1);
             mbar_init(bar_cs + i, 1);
             mbar_init(bar_csf + i, 128);
-            mbar_init(bar_p + i, 128);
+            mbar_init(bar_p + i, 256);  // both row halves
         }
         mbar_init(bar_pv, 1);
         mbar_init(bar_o, 1);
@@ -151,8 +154,9 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         q_row = k_row + (it % p.tiles) * 128;
     };
 
+    // registers: 8 softmax warps at 168, the 8 others at 88 (512 threads x 128 at launch)
     if (warp < 4) {
-        regs_dec<96>();
+        regs_dec<88>();
         if (warp == 0 && lane == 0) {
             // ---------------------------------------------------------- Q loader
             tma_prefetch_desc(&tm_q);
@@ -281,13 +285,18 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 if ((int)g + 2 < total) s_block(g + 2);  // into the buffer P_g just left
             }
         }
-    } else if (warp < 8) {
-        regs_inc<232>();
+    } else if (warp < 12) {
+        regs_inc<168>();
         // -------------------------------------------------------------- softmax + epilogue
-        const int quad = warp - 4;
+        // two warps per TMEM lane quadrant (warps 4 + q and 8 + q, both on SMSP q): half h
+        // owns key columns [64 h, 64 h + 64) of every block and O columns [E/2 h, E/2 h + E/2);
+        // the halves swap their block maxima through shared memory (64-thread named barrier
+        // per quadrant) and their row sums once per item
+        const int quad = warp & 3, hf = (warp - 4) >> 2;
         const int row = quad * 32 + lane;
+        const uint32_t bar_id = 1 + quad;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-        const uint32_t tO = tmem + lane_off + L::kOcol;
+        const uint32_t tO = tmem + lane_off + L::kOcol + hf * (E / 2);
         const float sl2 = p.qk_scale_log2;
         uint32_t g = 0, li = 0;
         for (int it = blockIdx.x; it < items; it += gridDim.x, ++li) {
@@ -304,27 +313,30 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 slot = (int)(tok / p.cs_chunk - ((int64_t)(it % p.tiles) * 128) / p.cs_chunk);
             }
             for (int j = 0; j < nblk; ++j, ++g) {
-                const int ncols = min(128, p.n - j * 128);
+                const int nh = min(64, max(0, p.n - j * 128 - 64 * hf));  // live columns of this half
                 const uint32_t tS = tmem + lane_off + (g & 1) * 128;
                 mbar_wait(bar_s + (g & 1), (g >> 1) & 1);
                 tc_fence_after();
-                uint32_t sr[128];
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    tmem_ld32(tS + q * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[q * 32]));
+                uint32_t sr[64];
+                tmem_ld32(tS + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+                tmem_ld32(tS + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
                 tmem_ld_wait();
-                if (ncols < 128) {
+                if (nh < 64) {
 #pragma unroll
-                    for (int i = 0; i < 128; ++i)
-                        if (i >= ncols) sr[i] = __float_as_uint(-INFINITY);
+                    for (int i = 0; i < 64; ++i)
+                        if (i >= nh) sr[i] = __float_as_uint(-INFINITY);
                 }
                 float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                for (int i = 0; i < 128; i += 8)
+                for (int i = 0; i < 64; i += 8)
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
                         mx4[u] = fmax3(mx4[u], __uint_as_float(sr[i + 2 * u]), __uint_as_float(sr[i + 2 * u + 1]));
-                const float mraw = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+                const float mloc = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+                float* xr = xch + ((g & 1) * 128 + row) * 2;
+                xr[hf] = mloc;
+                named_bar_sync(bar_id, 64);
+                const float mraw = fmaxf(mloc, xr[hf ^ 1]);
                 const float mx = row_ok ? mraw * sl2 : -INFINITY;
                 m_true = fmaxf(m_true, mx);
                 const bool need = mx > m_run + kRescaleThreshold;
@@ -338,9 +350,9 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 float2 part0 = make_float2(0.f, 0.f), part1 = make_float2(0.f, 0.f);
                 if (kCs && g >= 1) mbar_wait(bar_cs + ((g - 1) & 1), ((g - 1) >> 1) & 1);  // P/W smem free
 #pragma unroll
-                for (int cc = 0; cc < 4; ++cc) {
+                for (int cc = 0; cc < 2; ++cc) {
                     uint32_t pk[16];
-                    if (cc * 32 >= ncols) {
+                    if (cc * 32 >= nh) {
 #pragma unroll
                         for (int q = 0; q < 16; ++q) pk[q] = 0u;
                     } else {
@@ -361,14 +373,13 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                             pk[q] = pack_bf16x2(e.x, e.y);
                         }
                     }
-                    tmem_st16(tS + cc * 16, pk);
+                    tmem_st16(tS + hf * 32 + cc * 16, pk);  // P of keys 64 hf + 32 cc ..
                     if (kCs) {
-                        // the row's P copy (K-major, 128B-swizzled: strip cc / 2, 16-byte
-                        // chunks (cc % 2) * 4 .. + 3 of this row)
-                        uint8_t* rp = sp + (cc >> 1) * L::kStrip + row * 128;
+                        // the row's P copy (K-major, 128B-swizzled): strip hf, chunks cc * 4 ..
+                        uint8_t* rp = sp + hf * L::kStrip + row * 128;
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            const int ch = (cc & 1) * 4 + u;
+                            const int ch = cc * 4 + u;
                             *reinterpret_cast<uint4*>(rp + ((ch ^ (row & 7)) << 4)) =
                                 make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
                         }
@@ -377,27 +388,29 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 const float2 part = __fadd2_rn(part0, part1);
                 l_run += part.x + part.y;
                 if (kCs) {
-                    // W[slot][row] = w, W[1 - slot][row] = 0 (bf16, K-major 128B-swizzled rows)
-                    // stale stats far below the fresh logits: the reference's fp32 exp overflows
-                    // to +inf for the keys past ~88 nats (attention.cpp:135); a finite cap keeps
-                    // those products overflowing (p w -> +inf in the MMA) without turning the
-                    // masked p = 0 entries into inf * 0 = NaN
-                    const float w = row_ok ? fminf(ex2_approx(m_run - mpl) * inv_lp, 3.0e38f) : 0.f;
-                    const __nv_bfloat16 wb = __float2bfloat16_rn(w), zb = __float2bfloat16_rn(0.f);
-                    uint8_t* ws = sw + (row >> 6) * 2048;
-                    const int kc = (row & 63) >> 3, ke = row & 7;
+                    if (hf == 0) {
+                        // W[slot][row] = w, W[1 - slot][row] = 0 (bf16, K-major 128B-swizzled).
+                        // Stale stats far below the fresh logits: the reference's fp32 exp
+                        // overflows to +inf past ~88 nats (attention.cpp:135); a finite cap keeps
+                        // those products overflowing (p w -> +inf in the MMA) without turning the
+                        // masked p = 0 entries into inf * 0 = NaN
+                        const float w = row_ok ? fminf(ex2_approx(m_run - mpl) * inv_lp, 3.0e38f) : 0.f;
+                        const __nv_bfloat16 wb = __float2bfloat16_rn(w), zb = __float2bfloat16_rn(0.f);
+                        uint8_t* ws = sw + (row >> 6) * 2048;
+                        const int kc = (row & 63) >> 3, ke = row & 7;
 #pragma unroll
-                    for (int n = 0; n < 2; ++n)
-                        *reinterpret_cast<__nv_bfloat16*>(ws + n * 128 + (((kc ^ n) & 7) << 4) + ke * 2) =
-                            n == slot ? wb : zb;
+                        for (int n = 0; n < 2; ++n)
+                            *reinterpret_cast<__nv_bfloat16*>(ws + n * 128 + (((kc ^ n) & 7) << 4) + ke * 2) =
+                                n == slot ? wb : zb;
+                    }
                     fence_proxy_async_smem();  // generic smem writes -> the MMA's async proxy
                 }
                 if (j > 0 && __any_sync(0xffffffffu, need)) {
-                    // O holds P V of blocks < j once P_{g-1} V_{g-1} completed
+                    // O holds P V of blocks < j once P_{g-1} V_{g-1} completed; this half's columns
                     mbar_wait(bar_pv, (g - 1) & 1);
                     tc_fence_after();
 #pragma unroll 1
-                    for (int oc = 0; oc < E / 32; ++oc) {
+                    for (int oc = 0; oc < E / 64; ++oc) {
                         uint32_t r[32];
                         tmem_ld32(tO + oc * 32, r);
                         tmem_ld_wait();
@@ -411,37 +424,42 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 mbar_arrive(bar_p + (g & 1));
             }
             // ------------------------------------------------------------ epilogue
+            lxch[row * 2 + hf] = l_run;
+            named_bar_sync(bar_id, 64);
+            const float l_full = l_run + lxch[row * 2 + (hf ^ 1)];
             mbar_wait(bar_o, li & 1);
             tc_fence_after();
             {
-                uint32_t ro[E];
+                uint32_t ro[E / 2];
 #pragma unroll
-                for (int oc = 0; oc < E / 32; ++oc)
+                for (int oc = 0; oc < E / 64; ++oc)
                     tmem_ld32(tO + oc * 32, *reinterpret_cast<uint32_t(*)[32]>(&ro[oc * 32]));
                 tmem_ld_wait();
                 if (row_ok) {
-                    const float inv_l = 1.0f / l_run;
-                    uint4* dp = reinterpret_cast<uint4*>(p.out + sd_tok_off(p.layout, b, h, tok, p.heads, p.n, E));
+                    const float inv_l = 1.0f / l_full;
+                    uint4* dp = reinterpret_cast<uint4*>(p.out + sd_tok_off(p.layout, b, h, tok, p.heads, p.n, E) +
+                                                         hf * (E / 2));
 #pragma unroll
-                    for (int q = 0; q < E / 8; ++q)
+                    for (int q = 0; q < E / 16; ++q)
                         dp[q] = make_uint4(pack_bf16x2(__uint_as_float(ro[8 * q]) * inv_l, __uint_as_float(ro[8 * q + 1]) * inv_l),
                                            pack_bf16x2(__uint_as_float(ro[8 * q + 2]) * inv_l, __uint_as_float(ro[8 * q + 3]) * inv_l),
                                            pack_bf16x2(__uint_as_float(ro[8 * q + 4]) * inv_l, __uint_as_float(ro[8 * q + 5]) * inv_l),
                                            pack_bf16x2(__uint_as_float(ro[8 * q + 6]) * inv_l, __uint_as_float(ro[8 * q + 7]) * inv_l));
-                    if (p.row_max != nullptr) {
+                    if (hf == 0 && p.row_max != nullptr) {
                         const int64_t si = (int64_t)bh * p.n + tok;
                         p.row_max[si] = m_true * kLn2;
-                        p.exp_sum[si] = l_run * exp2f(m_run - m_true);
+                        p.exp_sum[si] = l_full * exp2f(m_run - m_true);
                     }
                 }
             }
+            named_bar_sync(bar_id, 64);  // lxch read by both halves before the next item's write
             tc_fence_before();  // O reads ordered before the next item's first bar_p arrive
         }
     } else {
-        regs_dec<96>();
+        regs_dec<88>();
         if (kCs) {
             // ---------------------------------------------------------- column-sum readers
-            const int quad = warp - 8;
+            const int quad = warp - 12;
             const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
             uint32_t g = 0;
             for (int it = blockIdx.x; it < items; it += gridDim.x) {
@@ -505,7 +523,8 @@ cudaError_t launch_sd(const AttnTcArgs& a, cudaStream_t s) {
     off = p.off_v + 2 * L::kKV;
     p.off_p = off;
     p.off_w = off + (cs ? L::kP : 0);
-    p.off_bar = p.off_w + (cs ? L::kW : 0);
+    p.off_x = p.off_w + (cs ? L::kW : 0);
+    p.off_bar = p.off_x + L::kXch;
     const uint32_t smem_bytes = p.off_bar + 256;
     if (smem_bytes > L::kMaxSmem) return cudaErrorNotSupported;
     if (cs) {
