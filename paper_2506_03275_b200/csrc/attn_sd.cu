@@ -78,7 +78,14 @@ struct SDParams {
     const float* prev_l;
     int cs_chunk, cs_chunks;
     float qk_scale_log2;
+    uint64_t* trace;  // debug timeline (null: off), 8 CTAs x 2048 clock64 stamps
 };
+
+#define SD_TRACE(ev, ix)                                                                     \
+    do {                                                                                     \
+        if (p.trace != nullptr && blockIdx.x < 8)                                            \
+            p.trace[blockIdx.x * 2048 + (ev) * 64 + ((ix) & 63)] = clock64();                \
+    } while (0)
 
 __device__ __forceinline__ int64_t sd_tok_off(int layout, int64_t b, int64_t h, int64_t tok,
                                               int heads, int n, int e) {
@@ -238,6 +245,7 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 want_q(g);
                 mbar_wait(bar_kf + (g & 1), (g >> 1) & 1);
                 tc_fence_after();
+                if (lane == 0) SD_TRACE(0, g);
                 issue_s(g);
                 if ((int)(g % nblk) == nblk - 1) commit(bar_qe);
             };
@@ -246,6 +254,7 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
             for (uint32_t g = 0; (int)g < total; ++g) {
                 const int j = (int)(g % nblk);
                 mbar_wait(bar_p + (g & 1), (g >> 1) & 1);
+                if (lane == 0) SD_TRACE(1, g);
                 mbar_wait(bar_vf + (g & 1), (g >> 1) & 1);
                 tc_fence_after();
                 {
@@ -317,6 +326,8 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 const uint32_t tS = tmem + lane_off + (g & 1) * 128;
                 mbar_wait(bar_s + (g & 1), (g >> 1) & 1);
                 tc_fence_after();
+                if (lane == 0 && warp == 4) SD_TRACE(2, g);
+                if (lane == 0 && warp == 8) SD_TRACE(3, g);
                 uint32_t sr[64];
                 tmem_ld32(tS + hf * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
                 tmem_ld32(tS + hf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
@@ -337,6 +348,7 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 xr[hf] = mloc;
                 named_bar_sync(bar_id, 64);
                 const float mraw = fmaxf(mloc, xr[hf ^ 1]);
+                if (lane == 0 && warp == 4) SD_TRACE(6, g);
                 const float mx = row_ok ? mraw * sl2 : -INFINITY;
                 m_true = fmaxf(m_true, mx);
                 const bool need = mx > m_run + kRescaleThreshold;
@@ -421,6 +433,8 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 }
                 tmem_st_wait();
                 tc_fence_before();
+                if (lane == 0 && warp == 4) SD_TRACE(4, g);
+                if (lane == 0 && warp == 8) SD_TRACE(5, g);
                 mbar_arrive(bar_p + (g & 1));
             }
             // ------------------------------------------------------------ epilogue
@@ -496,6 +510,8 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     }
 }
 
+uint64_t* h_sd_trace = nullptr;
+
 template <int E>
 cudaError_t launch_sd(const AttnTcArgs& a, cudaStream_t s) {
     using L = SDLayout<E>;
@@ -516,6 +532,7 @@ cudaError_t launch_sd(const AttnTcArgs& a, cudaStream_t s) {
     p.row_max = a.row_max;
     p.exp_sum = a.exp_sum;
     p.qk_scale_log2 = kLog2e / std::sqrt((float)E);
+    p.trace = h_sd_trace;
     const bool cs = a.colsum != nullptr;
     uint32_t off = L::kQ;
     p.off_k = off;
@@ -572,3 +589,9 @@ cudaError_t attn_sd(const AttnTcArgs& a, cudaStream_t s) {
 
 }  // namespace dev
 }  // namespace csd
+
+// Debug only: clock64 timeline of k_attn_sd's first 8 CTAs (8 x 2048 uint64; null: off).
+extern "C" int csd_debug_set_attn_sd_trace(void* dev_buf) {
+    csd::dev::h_sd_trace = static_cast<uint64_t*>(dev_buf);
+    return 0;
+}
