@@ -897,6 +897,26 @@ bool make_map_bf16(CUtensorMap* m, const void* base, uint64_t cols, uint64_t row
     return r == CUDA_SUCCESS;
 }
 
+// General 2-D map: element size 2 (bf16) or 4 (fp32), box {box_cols, box_rows}, the given
+// swizzle (box_cols * elem_bytes must equal the swizzle span for the swizzled modes).
+bool make_map_2d(CUtensorMap* m, const void* base, int elem_bytes, uint64_t cols, uint64_t rows,
+                 uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows, int swizzle_bytes) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {pitch_elems * (uint64_t)elem_bytes};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                        : CU_TENSOR_MAP_SWIZZLE_NONE;
+    CUresult r = fn(m, elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 bool attn_tc_supported(int64_t e, int64_t chunk) {
     return (e == 64 || e == 128) && chunk >= 1 && chunk <= 256;
 }

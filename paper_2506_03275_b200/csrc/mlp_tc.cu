@@ -30,6 +30,8 @@ using namespace csd::tc;
 
 bool make_map_bf16(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows,
                    uint64_t pitch_elems, uint32_t box_rows);
+bool make_map_2d(CUtensorMap* m, const void* base, int elem_bytes, uint64_t cols, uint64_t rows,
+                 uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows, int swizzle_bytes);
 
 // Debug timeline (scripts/mlp_trace.py): CTAs with blockIdx.y == 0 and blockIdx.x < 8
 // record clock64() at fixed slots when the pointer is set.
@@ -389,23 +391,41 @@ k_smlp_up(const __grid_constant__ CUtensorMap tm_x, const MlpParams p) {
 // x_out = x_mid + M_cache (north_star item 5: the cache update fused into the epilogue).
 // The TMEM accumulator is double-buffered so an item's epilogue overlaps the next item's
 // K loop.  Stage = delta tile (TMA) + 64 gathered W2 rows x 128 columns (cp.async, MN-major).
-constexpr int kDnStages = 3;
+//
+// Epilogue through TMA: an item's 128 columns are four 32-column slices; each slice's
+// M_cache rows (fp32, 128 B per row, 128B swizzle) and x_mid rows (bf16, 64 B, 64B swizzle)
+// are TMA-loaded into one of two slice buffers ahead of use (the loads do not depend on the
+// accumulator, so they run ahead of the K loop), updated in place by thread = chunk row
+// (the swizzles keep a warp's 16-byte accesses conflict-free), and TMA-stored back.  The
+// read-modify-write is then bound by the TMA engine's bytes in flight, not by the
+// per-thread register budget of a load -> use -> store loop.
 template <int NT>
 struct DnLayout {
     static constexpr uint32_t kStage = NT * kTile + kTile;  // A (rows x 64 k) + B (64 k x 128)
-    static constexpr uint32_t kStg = kStage * kDnStages;    // epilogue transposition buffers
-    static constexpr uint32_t kStgBytes = 4 * NT * 4096;     // one 32 x 32 fp32 block per warp
-    static constexpr uint32_t kBar = kStg + kStgBytes;
-    static constexpr uint32_t kAlloc = kBar + 256 + 1024;
     // warps 0 (TMA + copy), 1 (MMA), 2-3 (copy), 4 .. 4 + 4 NT - 1 (epilogue), then 4 more
     // copy warps: the W2 row gather (cp.async, LSU rate per issuing warp) is the K loop's limiter
     static constexpr uint32_t kThreads = 256 + 128 * NT;
     static constexpr uint32_t kTmemCols = 2 * NT * 128 <= 256 ? 256 : 512;
+    static constexpr uint32_t kMaxSmem = 227 * 1024;
+    static constexpr uint32_t kBarBytes = 256;
+    __host__ __device__ static constexpr uint32_t ebuf_m(int chunk) { return ((uint32_t)chunk * 128u + 1023u) & ~1023u; }
+    __host__ __device__ static constexpr uint32_t ebuf_x(int chunk) { return ((uint32_t)chunk * 64u + 1023u) & ~1023u; }
+    __host__ __device__ static constexpr uint32_t ebytes(int chunk) { return 2u * (ebuf_m(chunk) + ebuf_x(chunk)); }
+    __host__ __device__ static constexpr int stages(int chunk) {
+        return (4 * kStage + ebytes(chunk) + kBarBytes + 1024 <= kMaxSmem)   ? 4
+               : (3 * kStage + ebytes(chunk) + kBarBytes + 1024 <= kMaxSmem) ? 3
+                                                                             : 2;
+    }
+    __host__ __device__ static constexpr uint32_t alloc(int chunk) {
+        return stages(chunk) * kStage + ebytes(chunk) + kBarBytes + 1024;
+    }
 };
 
 template <int NT>
 __global__ void __launch_bounds__(DnLayout<NT>::kThreads, 1)
-k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
+k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const __grid_constant__ CUtensorMap tm_mc,
+            const __grid_constant__ CUtensorMap tm_xm, const __grid_constant__ CUtensorMap tm_xo,
+            const MlpParams p) {
     using L = DnLayout<NT>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -413,23 +433,27 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntd = p.d / 128;
     const int items = p.nz * ntd;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
-    uint64_t* full = bars;                    // [kDnStages]
-    uint64_t* empty = bars + kDnStages;       // [kDnStages]
-    uint64_t* tfull = bars + 2 * kDnStages;   // [2] accumulator buffer final
-    uint64_t* tempty = tfull + 2;             // [2] accumulator buffer drained
-    uint32_t* slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    const int nst = L::stages(p.chunk);
+    uint8_t* ebase = smem + nst * L::kStage;  // [2] M slices, then [2] x slices
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ebase + L::ebytes(p.chunk));
+    uint64_t* full = bars;           // [4]
+    uint64_t* empty = bars + 4;      // [4]
+    uint64_t* tfull = bars + 8;      // [2] accumulator buffer final
+    uint64_t* tempty = tfull + 2;    // [2] accumulator buffer drained
+    uint64_t* efull = tempty + 2;    // [2] epilogue slice buffer loaded
+    uint32_t* slot = reinterpret_cast<uint32_t*>(efull + 2);
     constexpr int kCopyThreads = 224;         // warps 0, 2, 3 and the 4 trailing warps
     constexpr int kXtra = 4 + 4 * NT;         // first trailing copy warp
     if (threadIdx.x == 0) {
-        if (blockIdx.x == 0) MLP_TRACE(200);
-        for (int s = 0; s < kDnStages; ++s) {
+        MLP_TRACE(200);
+        for (int s = 0; s < nst; ++s) {
             mbar_init(full + s, 1 + kCopyThreads);
             mbar_init(empty + s, 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(tfull + i, 1);
             mbar_init(tempty + i, 128 * NT);
+            mbar_init(efull + i, 1);
         }
         fence_barrier_init();
     }
@@ -455,7 +479,7 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
             const int kbs = (cnt + 63) / 64;
             const int32_t* ids = p.idx + (int64_t)z * p.k_max;
             for (int kb = 0; kb < kbs; ++kb, ++gk) {
-                const int s = gk % kDnStages;
+                const int s = gk % nst;
                 int nid[kPer];
 #pragma unroll
                 for (int i = 0; i < kPer; ++i) {
@@ -463,7 +487,7 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
                     int nn = kb * 64 + ((idx >> 4) & 63);
                     nid[i] = __ldg(ids + (nn < cnt ? nn : cnt - 1));  // pad: a valid row (delta = 0)
                 }
-                if (gk >= kDnStages) mbar_wait(empty + s, ((gk / kDnStages) - 1) & 1);
+                if (gk >= (uint32_t)nst) mbar_wait(empty + s, ((gk / nst) - 1) & 1);
                 if (warp == 0 && lane == 0) {
                     const int nbox = (p.chunk + 63) >> 6;  // only the chunk's rows
                     mbar_arrive_expect_tx(full + s, (uint32_t)nbox * 8192u);
@@ -502,11 +526,11 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
                     continue;
                 }
                 for (int kb = 0; kb < kbs; ++kb, ++gk) {
-                    const int s = gk % kDnStages;
-                    mbar_wait(full + s, (gk / kDnStages) & 1);
+                    const int s = gk % nst;
+                    mbar_wait(full + s, (gk / nst) & 1);
                     fence_proxy_async_smem();  // cp.async (generic proxy) data -> tcgen05 reads
                     tc_fence_after();
-                    if (blockIdx.x == 0 && li == 0) MLP_TRACE(202 + kb);
+                    if (kb == 0 && li < 8) MLP_TRACE(202 + 2 * li);
                     const uint32_t sa = s0 + s * L::kStage, sb = sa + NT * kTile;
                     for (int t = 0; t < NT; ++t) {
 #pragma unroll
@@ -518,31 +542,55 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
                     mma_commit(empty + s);
                 }
                 mma_commit(tfull + ab);
+                if (li < 8) MLP_TRACE(203 + 2 * li);
             }
         }
     } else {
         // setmaxnreg.inc draws only on registers this CTA's decs released (8 warps x 56 at
         // 128 -> 72 fund exactly 8 warps x 56 at 128 -> 184); asking for more deadlocks
         if constexpr (NT == 2) regs_inc<184>();
-        // epilogue warps: thread = chunk row for the TMEM read; each warp then transposes
-        // 32 x 32 fp32 blocks through its own smem slice so the M_cache read-modify-write and
-        // the residual run row-contiguously (8 lanes x 16 B per 32-column row segment)
         const int sw = warp - 4, t = sw >> 2, quad = warp & 3;
-        const int r = t * 128 + quad * 32 + lane;
-        float* stg = reinterpret_cast<float*>(smem + L::kStg + sw * 4096);
-        const bool warp_live = t * 128 + quad * 32 < p.chunk;
-        uint32_t li = 0;
-        for (int item = blockIdx.x; item < items; item += gridDim.x, ++li) {
+        const int r = t * 128 + quad * 32 + lane;  // chunk row (TMEM lane)
+        const bool row_ok = r < p.chunk;
+        const bool lead = sw == 0 && lane == 0;  // issues the slice loads and stores
+        const bool has_x = p.x_out != nullptr;
+        const uint32_t em = L::ebuf_m(p.chunk), ex = L::ebuf_x(p.chunk);
+        const uint32_t tx_bytes = (uint32_t)p.chunk * (has_x ? 192u : 128u);
+        const int my_items = (items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+        const int nslices = my_items * 4;
+        auto slice_rc = [&](int sl, int& col, int& row0) {
+            const int item = blockIdx.x + (sl >> 2) * gridDim.x;
             const int z = item / ntd, td = item - z * ntd;
+            const int b = z / p.chunks, c = z - b * p.chunks;
+            col = td * 128 + (sl & 3) * 32;
+            row0 = b * p.n + c * p.chunk;
+        };
+        auto issue = [&](int sl) {  // lead only: load slice sl into buffer sl & 1
+            if (sl >= nslices) return;
+            int col, row0;
+            slice_rc(sl, col, row0);
+            const int bi = sl & 1;
+            mbar_arrive_expect_tx(efull + bi, tx_bytes);
+            tma_load_2d(&tm_mc, efull + bi, ebase + bi * em, col, row0);
+            if (has_x) tma_load_2d(&tm_xm, efull + bi, ebase + 2 * em + bi * ex, col, row0);
+        };
+        if (lead) {
+            tma_prefetch_desc(&tm_mc);
+            if (has_x) { tma_prefetch_desc(&tm_xm); tma_prefetch_desc(&tm_xo); }
+            issue(0);
+            issue(1);
+        }
+        uint32_t li = 0;
+        int sl = 0;
+        for (int item = blockIdx.x; item < items; item += gridDim.x, ++li) {
+            const int z = item / ntd;
             const bool has_acc = p.counts[z] > 0;
             const uint32_t ab = li & 1;
             mbar_wait(tfull + ab, (li >> 1) & 1);
             tc_fence_after();
-            if (blockIdx.x == 0 && sw == 0 && lane == 0 && li == 0) MLP_TRACE(230);
+            if (sw == 0 && lane == 0 && li < 8) MLP_TRACE(230 + 2 * li);
             const uint32_t tacc = tmem + ab * (NT * 128) + ((uint32_t)(quad * 32) << 16) + t * 128;
-            const int b = z / p.chunks, c = z - b * p.chunks;
-            const int64_t row0 = (int64_t)b * p.n + (int64_t)c * p.chunk + t * 128 + quad * 32;
-            for (int oc = 0; oc < 4; ++oc) {
+            for (int oc = 0; oc < 4; ++oc, ++sl) {
                 uint32_t v[32];
                 if (has_acc) {
                     tmem_ld32(tacc + oc * 32, v);
@@ -555,51 +603,58 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const MlpParams p) {
                     tc_fence_before();
                     mbar_arrive(tempty + ab);
                 }
-                if (!warp_live) continue;
-                __syncwarp();
+                const int bi = sl & 1;
+                mbar_wait(efull + bi, (sl >> 1) & 1);
+                if (row_ok) {
+                    // M row: 8 x 16 B at chunk position q ^ (r & 7) (128B swizzle)
+                    float* mrow = reinterpret_cast<float*>(ebase + bi * em + r * 128);
+                    float mv[32];
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    *reinterpret_cast<uint4*>(stg + lane * 32 + ((q ^ (lane & 7)) << 2)) =
-                        make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                __syncwarp();
-                // lane -> (row rr = it * 4 + lane / 8, columns 4 (lane % 8) .. + 3); all the
-                // round's global loads are issued before any use (8 rows in flight per lane)
-                const int c4 = lane & 7;
-                const int col = td * 128 + oc * 32 + c4 * 4;
-                const int rlim = p.chunk - (t * 128 + quad * 32);  // live rows of this warp
-                float4 m[8];
-                uint2 xm[8];
+                    for (int q = 0; q < 8; ++q) {
+                        float4* pm = reinterpret_cast<float4*>(mrow + ((q ^ (r & 7)) << 2));
+                        float4 a = *pm;
+                        a.x += __uint_as_float(v[4 * q]);
+                        a.y += __uint_as_float(v[4 * q + 1]);
+                        a.z += __uint_as_float(v[4 * q + 2]);
+                        a.w += __uint_as_float(v[4 * q + 3]);
+                        *pm = a;
+                        mv[4 * q] = a.x;
+                        mv[4 * q + 1] = a.y;
+                        mv[4 * q + 2] = a.z;
+                        mv[4 * q + 3] = a.w;
+                    }
+                    if (has_x) {
+                        // x row: 4 x 16 B at chunk position q ^ ((r >> 1) & 3) (64B swizzle)
+                        uint4* xrow = reinterpret_cast<uint4*>(ebase + 2 * em + bi * ex + r * 64);
 #pragma unroll
-                for (int it = 0; it < 8; ++it) {
-                    const int rr = it * 4 + (lane >> 3);
-                    if (rr < rlim) {
-                        const int64_t go = (row0 + rr) * p.d + col;
-                        m[it] = *reinterpret_cast<const float4*>(p.out_cache + go);
-                        if (p.x_out != nullptr) xm[it] = *reinterpret_cast<const uint2*>(p.x_mid + go);
+                        for (int q = 0; q < 4; ++q) {
+                            uint4* px = xrow + (q ^ ((r >> 1) & 3));
+                            uint4 xv = *px;
+                            uint32_t* w = reinterpret_cast<uint32_t*>(&xv);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[u]));
+                                w[u] = pack_bf16x2(f.x + mv[8 * q + 2 * u], f.y + mv[8 * q + 2 * u + 1]);
+                            }
+                            *px = xv;
+                        }
                     }
                 }
-#pragma unroll
-                for (int it = 0; it < 8; ++it) {
-                    const int rr = it * 4 + (lane >> 3);
-                    if (rr >= rlim) continue;
-                    const float4 a = *reinterpret_cast<const float4*>(stg + rr * 32 + ((c4 ^ (rr & 7)) << 2));
-                    const int64_t go = (row0 + rr) * p.d + col;
-                    float4 mm = m[it];
-                    mm.x += a.x;
-                    mm.y += a.y;
-                    mm.z += a.z;
-                    mm.w += a.w;
-                    *reinterpret_cast<float4*>(p.out_cache + go) = mm;
-                    if (p.x_out != nullptr) {
-                        const float2 x0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xm[it].x));
-                        const float2 x1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xm[it].y));
-                        *reinterpret_cast<uint2*>(p.x_out + go) =
-                            make_uint2(pack_bf16x2(x0.x + mm.x, x0.y + mm.y), pack_bf16x2(x1.x + mm.z, x1.y + mm.w));
-                    }
+                fence_proxy_async_smem();  // generic-proxy smem writes -> the TMA store
+                named_bar_sync(1, 128 * NT);
+                if (lead) {
+                    int col, row0;
+                    slice_rc(sl, col, row0);
+                    tma_store_2d(&tm_mc, ebase + bi * em, col, row0);
+                    if (has_x) tma_store_2d(&tm_xo, ebase + 2 * em + bi * ex, col, row0);
+                    bulk_commit();
+                    bulk_wait_read0();  // the store has read buffer bi: reuse it
+                    issue(sl + 2);
                 }
             }
-            if (blockIdx.x == 0 && sw == 0 && lane == 0 && li == 0) MLP_TRACE(231);
+            if (sw == 0 && lane == 0 && li < 8) MLP_TRACE(231 + 2 * li);
         }
+        if (lead) bulk_wait0();
     }
     tc_fence_before();
     __syncthreads();
@@ -627,9 +682,13 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
     const int64_t nc = n / chunk;
     int tn_width = 0, ntiles = 0;
     smlp_geometry(k_max, batch * nc, &tn_width, &ntiles, nullptr);
-    CUtensorMap tx, tdl;
+    CUtensorMap tx, tdl, tmc, txm, txo;
+    const uint64_t rows_all = (uint64_t)(batch * n);
     if (!make_map_bf16(&tx, x, d, batch * n, d, 64) ||
-        !make_map_bf16(&tdl, delta_ws, k_pad, batch * nc * chunk, k_pad, 64))
+        !make_map_bf16(&tdl, delta_ws, k_pad, batch * nc * chunk, k_pad, 64) ||
+        !make_map_2d(&tmc, out_cache, 4, d, rows_all, d, 32, (uint32_t)chunk, 128) ||
+        !make_map_2d(&txm, x_mid != nullptr ? x_mid : x, 2, d, rows_all, d, 32, (uint32_t)chunk, 64) ||
+        !make_map_2d(&txo, x_out != nullptr ? x_out : x, 2, d, rows_all, d, 32, (uint32_t)chunk, 64))
         return cudaErrorInvalidValue;
     MlpParams p{};
     p.trace = h_mlp_trace;
@@ -654,7 +713,7 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
     p.nz = (int)(batch * nc);
     {
         cudaError_t e = ensure_smem_attr(k_smlp_up<NT>, (int)LU::kMaxSmem);
-        if (e == cudaSuccess) e = ensure_smem_attr(k_smlp_down<NT>, (int)DnLayout<NT>::kAlloc);
+        if (e == cudaSuccess) e = ensure_smem_attr(k_smlp_down<NT>, (int)DnLayout<NT>::kMaxSmem);
         if (e != cudaSuccess) return e;
     }
     dim3 g1((unsigned)ntiles, (unsigned)(batch * nc));
@@ -664,7 +723,7 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
     const int sms = sm_count();
     const int64_t items = batch * nc * (d / 128);
     k_smlp_down<NT><<<(unsigned)std::min<int64_t>(items, sms), DnLayout<NT>::kThreads,
-                      DnLayout<NT>::kAlloc, s>>>(tdl, p);
+                      DnLayout<NT>::alloc((int)chunk), s>>>(tdl, tmc, txm, txo, p);
     return cudaGetLastError();
 }
 

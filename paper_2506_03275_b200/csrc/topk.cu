@@ -325,20 +325,41 @@ k_topk_cluster(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* 
     const int64_t wseg = (nloc + kTopkWarps - 1) / kTopkWarps;  // per-warp sub-segment
     const int64_t w0 = min(nloc, warp * wseg), w1 = min(nloc, w0 + wseg);
     uint32_t kand = 0xffffffffu, kor = 0u;
-    for (int64_t j = w0 + lane; j < w1; j += 32) {
-        float sc;
+    // kU elements per lane per round, every load of the round issued before the first use
+    // (the scores are an L2-latency-bound read: one round covers FLUX's 192 per warp)
+    constexpr int kU = 8;
+    for (int64_t jb = w0 + lane; jb < w1; jb += 32 * kU) {
+        float sc[kU];
         if constexpr (kFused) {
-            const int64_t e = row * m + c0 + j, total = (int64_t)gridDim.x / CS * m;
-            float acc = fs.partial[e];
-            for (int q = 1; q < fs.ks; ++q) acc += fs.partial[(int64_t)q * total + e];
-            sc = fabsf(acc - fs.cached[e]);
+            const int64_t total = (int64_t)gridDim.x / CS * m, e0 = row * m + c0 + jb;
+            float cv[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const bool ok = jb + u * 32 < w1;
+                sc[u] = ok ? __ldg(fs.partial + e0 + u * 32) : 0.f;
+                cv[u] = ok ? __ldg(fs.cached + e0 + u * 32) : 0.f;
+            }
+            for (int q = 1; q < fs.ks; ++q) {
+                const float* pq = fs.partial + (int64_t)q * total + e0;
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                    if (jb + u * 32 < w1) sc[u] += __ldg(pq + u * 32);
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) sc[u] = fabsf(sc[u] - cv[u]);
         } else {
-            sc = src[c0 + j];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) sc[u] = jb + u * 32 < w1 ? __ldg(src + c0 + jb + u * 32) : 0.f;
         }
-        const uint32_t o = ord_key(sc);
-        keys[j] = o;
-        kand &= o;
-        kor |= o;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            if (jb + u * 32 < w1) {
+                const uint32_t o = ord_key(sc[u]);
+                keys[jb + u * 32] = o;
+                kand &= o;
+                kor |= o;
+            }
+        }
     }
     kand = __reduce_and_sync(0xffffffffu, kand);
     kor = __reduce_or_sync(0xffffffffu, kor);
