@@ -968,6 +968,10 @@ static cudaError_t launch_attn(const AttnTcArgs& a, cudaStream_t s) {
     p.span = h_attn_span;
     p.cs_chunk = (a.colsum != nullptr && a.cs_chunk > 0 && a.cs_chunk != a.chunk) ? (int)a.cs_chunk : 0;
     p.cs_chunks = p.cs_chunk ? (int)(a.n / a.cs_chunk) : 0;
+    if (p.cs_chunk) {  // items straddle colsum chunks: the two partial sums are atomically merged
+        cudaError_t e = cudaMemsetAsync(a.colsum, 0, sizeof(float) * a.batch * a.heads * p.cs_chunks * a.n, s);
+        if (e != cudaSuccess) return e;
+    }
     p.items = (int)(a.batch * a.heads * p.chunks);
     p.qk_scale_log2 = kLog2e / std::sqrt((float)E);
 

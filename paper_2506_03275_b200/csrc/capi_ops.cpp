@@ -200,9 +200,7 @@ csd_status csd_column_sum_attention(csd_ctx* ctx, csd_mode mode, csd_layout layo
         // keeps every item within two chunks (the kernel's order-independent atomic merge)
         if (chunk >= 128 && chunk < 256 && chunk % 32 == 0 && n % 256 == 0) {
             a.chunk = 256;
-            a.cs_chunk = chunk;
-            CSD_CU(cudaMemsetAsync(column_sums, 0,
-                                   sizeof(float) * batch * heads * (n / chunk) * n, s), "memset");
+            a.cs_chunk = chunk;  // the kernels that merge partial column sums zero the buffer
         }
         if (prev_m == nullptr) {
             // first dense step: exact probabilities need the final stats first
