@@ -28,6 +28,10 @@ CU_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                    "-I", INCLUDE, "-I", CSRC, "--expt-relaxed-constexpr"]
 PER_FILE = {
     # bit-exact reference arithmetic: no FMA contraction, IEEE div/sqrt, denormals kept
+    # debug timelines compiled out of the production build (CSD_TRACE=1 builds them in): the
+    # predicated stamps cost 4 us of instruction fetch in the CTA-pair attention kernel
+    "attn_cp.cu": [] if os.environ.get("CSD_TRACE") else ["-DCSD_CP_NOTRACE"],
+    "attn_pp.cu": [] if os.environ.get("CSD_TRACE") else ["-DCSD_PP_NOTRACE"],
     "check_kernels.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false"],
     # the CHECK latent update is the reference's separate multiply and add
     "generation.cu": ["-fmad=false"],

@@ -90,16 +90,35 @@ struct PPParams {
 // Debug timeline (scripts/attn_pp_trace.py): CTAs < kPPTraceCtas stamp clock64() at slot (of 2048)
 // event * 64 + (index & 63); the pointer travels in the parameters (constant bank).
 constexpr int kPPTraceCtas = 8;
+#ifdef CSD_PP_NOTRACE
+#define PP_TRACE(ev, ix) \
+    do {                 \
+    } while (0)
+#else
 #define PP_TRACE(ev, ix)                                                                     \
     do {                                                                                     \
         if (p.trace != nullptr && blockIdx.x < kPPTraceCtas)                                 \
             p.trace[blockIdx.x * 2048 + (ev) * 64 + ((ix) & 63)] = clock64();                \
     } while (0)
+#endif
 
 __device__ __forceinline__ int64_t pp_tok_off(int layout, int64_t b, int64_t h, int64_t tok,
                                               int heads, int n, int e) {
     return layout == CSD_LAYOUT_BHNE ? (((b * heads + h) * (int64_t)n) + tok) * e
                                      : ((b * (int64_t)n + tok) * heads + h) * e;
+}
+
+// predicated 16-byte stores (the dry warm-up pass runs the epilogue code without storing;
+// inline PTX keeps the compiler from unswitching the loop into a second, store-free copy)
+__device__ __forceinline__ void st_shared_v4_if(bool on, void* ptr, const uint32_t (&v)[4]) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %5, 0;\n @p st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n}"
+                 ::"r"(smem_u32(ptr)), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"((int)on)
+                 : "memory");
+}
+__device__ __forceinline__ void st_global_v4_if(bool on, void* ptr, const uint4& v) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %5, 0;\n @p st.global.v4.b32 [%0], {%1, %2, %3, %4};\n}"
+                 ::"l"(ptr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"((int)on)
+                 : "memory");
 }
 
 __device__ __forceinline__ uint64_t pp_globaltimer() {
@@ -205,6 +224,7 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     int cp_it = items, cp_cnt = 0;
     int32_t cp_id[kCpRows];
     if (cpa && (warp == 2 || warp == 3 || warp >= 12)) {
+        pdl_wait();  // the counts / indices may come from the previous kernel (dense step top-k)
         cp_it = next_live(blockIdx.x, cp_cnt);
         load_ids(cp_it, cp_cnt, 0, cp_id);
     }
@@ -216,6 +236,8 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
 
     if (warp < 4 || warp >= 12) {
         regs_dec<72>();
+        pdl_wait();
+        if (threadIdx.x == 0) pdl_trigger();
         if (warp == 0) {
             if (lane == 0) {
                 // ---------------------------------------------------- Q loader (per tile)
@@ -510,24 +532,35 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         const int row = quad * 32 + lane;  // TMEM lane = row of tile t
         const int crow = t * 128 + row;    // row within the item
         const bool row_ok = row < rows_t;
-        // Warps holding no live row (tile 1 of a 192-row chunk) run the first item's key
-        // blocks once as an instruction-cache warm-up: no barrier waits or arrivals, their
-        // P stores land in dead TMEM lanes whose O rows are never read.  The cold first pass
-        // through the unrolled softmax costs ~8k cycles per block otherwise (L2 instruction
-        // fetches), on every CTA's critical path.
+        // Code warm-up (p.warm): before its first real item a softmax warp runs one DRY item
+        // through the same code -- two key blocks (a full and a partial one) and the
+        // epilogue -- with every barrier wait / arrive and every memory store switched off
+        // and its P stores aimed at O (rewritten by the first P V, which waits for this
+        // warp's real bar_p arrive).  The first pass through the unrolled softmax and
+        // epilogue otherwise costs ~15k cycles of instruction fetches on every CTA's
+        // critical path (worse after a GEMM evicted the code from L2).  warm 1: only the
+        // warps holding no live row (tile 1 of a 192-row chunk) run it, concurrently with
+        // the live warps' wait for their first S; warm 2: every softmax warp does.
         const bool live = quad * 32 < rows_t;
-        if (live || p.warm) {
+        bool dry = p.warm >= 2 || (p.warm == 1 && !live);
+        if (live || dry) {
             const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
             const uint32_t tS = tmem + lane_off + t * 128;
             const uint32_t tO = tmem + lane_off + L::kOcol + t * E;
             const float sl2 = p.qk_scale_log2;
             const bool has_base = p.base != nullptr;
             uint32_t g = 0, li = 0;
-            int cnt_nx = blockIdx.x < items ? count_of(blockIdx.x) : 0;
-            for (int it = blockIdx.x; it < items; it += gridDim.x) {
-                const int cnt = cnt_nx;  // loaded one item ahead
-                if (it + (int)gridDim.x < items) cnt_nx = count_of(it + gridDim.x);
-                const int item = item_at(it);
+            int cnt_nx = 0;
+            bool waited = false;  // the dry pass reads no global memory: it runs before pdl_wait
+            for (int it = blockIdx.x; it < items;) {
+                if (!dry && !waited) {
+                    pdl_wait();
+                    waited = true;
+                    cnt_nx = count_of(it);
+                }
+                const int cnt = dry ? 128 + 67 : cnt_nx;  // next count loaded one item ahead
+                if (!dry && it + (int)gridDim.x < items) cnt_nx = count_of(it + gridDim.x);
+                const int item = dry ? it : item_at(it);
                 const int c = item % p.chunks, bh = item / p.chunks;
                 const int b = bh / p.heads, h = bh % p.heads;
                 const int64_t tok = (int64_t)c * p.chunk + crow;
@@ -539,13 +572,16 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
 #pragma unroll
                         for (int q = 0; q < E / 8; ++q) dst[q] = src[q];
                     }
+                    it += gridDim.x;
                     continue;
                 }
+                const bool wait = live && !dry;
+                const uint32_t tP = dry ? tO : tS;  // P destination
                 const int nblk = (cnt + 127) / 128;
                 float m_run = -INFINITY, m_true = -INFINITY, l_run = 0.f;
-                for (int j = 0; j < nblk; ++j, ++g) {
+                for (int j = 0; j < nblk; ++j) {
                     const int ncols = min(128, cnt - j * 128);
-                    if (live) mbar_wait(bar_s + t, g & 1);
+                    if (wait) mbar_wait(bar_s + t, g & 1);
                     tc_fence_after();
                     if (threadIdx.x == 128 * (t + 1)) PP_TRACE(7 + 2 * t, g);
                     uint32_t sr[128];
@@ -606,7 +642,7 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                         }
                         // P_t (bf16 pairs) over S_t columns [16 cc, 16 cc + 16): every S
                         // column of this block is already in registers
-                        tmem_st16(tS + cc * 16, pk);
+                        tmem_st16(tP + cc * 16, pk);
                     }
                     const float2 part = __fadd2_rn(part0, part1);
                     l_run += part.x + part.y;
@@ -629,18 +665,20 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                     tmem_st_wait();
                     tc_fence_before();
                     if (threadIdx.x == 128 * (t + 1)) PP_TRACE(8 + 2 * t, g);
-                    if (live) mbar_arrive(bar_p + t);
+                    if (wait) {
+                        mbar_arrive(bar_p + t);
+                        ++g;
+                    }
                 }
-                if (!live) break;
                 // -------------------------------------------------------- epilogue
-                mbar_wait(bar_o + t, li & 1);
+                if (wait) mbar_wait(bar_o + t, li & 1);
                 tc_fence_after();
                 if (threadIdx.x == 128 * (t + 1)) PP_TRACE(11 + t, 2 * li);
                 if (p.stage_base) {
                     // out = base + scale * O / l with the item's base tile in smem (TMA,
                     // issued after the previous item's out store); rows combined in place,
                     // the I/O thread stores the tile by TMA
-                    mbar_wait(bar_bf, li & 1);
+                    if (wait) mbar_wait(bar_bf, li & 1);
                     const float fsc = p.scale / l_run;
                     uint32_t ro[E];
 #pragma unroll
@@ -665,12 +703,12 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                                 o4[u] = pack_bf16x2(fmaf(fsc, __uint_as_float(r[q * 8 + 2 * u]), f.x),
                                                     fmaf(fsc, __uint_as_float(r[q * 8 + 2 * u + 1]), f.y));
                             }
-                            *ptr = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+                            st_shared_v4_if(!dry, ptr, o4);  // dry pass: no store
                         }
                     }
                     fence_proxy_async_smem();  // in-place writes -> async proxy (TMA store)
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(bar_xc);
+                    if (lane == 0 && wait) mbar_arrive(bar_xc);
                 } else {
                     const int64_t off = pp_tok_off(p.layout, b, h, tok, p.heads, p.n, E);
                     const float inv_l = 1.0f / l_run;
@@ -709,18 +747,24 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                             v.y = pack_bf16x2(o[2], o[3]);
                             v.z = pack_bf16x2(o[4], o[5]);
                             v.w = pack_bf16x2(o[6], o[7]);
-                            dp[q] = v;
+                            st_global_v4_if(!dry, dp + q, v);
                         }
                     }
                 }
-                if (row_ok && p.row_max != nullptr) {
+                if (row_ok && !dry && p.row_max != nullptr) {
                     const int64_t si = (int64_t)bh * p.n + tok;
                     p.row_max[si] = m_true * kLn2;
                     p.exp_sum[si] = l_run * exp2f(m_run - m_true);
                 }
                 tc_fence_before();  // O reads ordered before the next item's bar_p arrive
                 if (threadIdx.x == 128 * (t + 1)) PP_TRACE(11 + t, 2 * li + 1);
+                if (dry) {  // the real items follow (a warp without live rows is done)
+                    dry = false;
+                    if (!live) break;
+                    continue;
+                }
                 ++li;
+                it += gridDim.x;
             }
         }
     }
@@ -811,8 +855,7 @@ cudaError_t launch_pp(const AttnTcArgs& a, cudaStream_t s) {
     cudaError_t err = ensure_smem_attr(kern, (int)L::kMaxSmem);
     if (err != cudaSuccess) return err;
     const unsigned grid = (unsigned)std::min<int64_t>(p.items, sm_count());
-    kern<<<grid, L::kThreads, smem_bytes, s>>>(tq, tk, tv, tb, to, p);
-    return cudaGetLastError();
+    return launch_ex(kern, dim3(grid), dim3(L::kThreads), smem_bytes, s, 1, tq, tk, tv, tb, to, p);
 }
 
 }  // namespace

@@ -154,6 +154,8 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    if (threadIdx.x == 0) pdl_trigger();
     auto item_rows = [&](int it, int& q_row, int& k_row, int& col0) {
         const int bh = it / p.tiles;
         k_row = p.layout == CSD_LAYOUT_BHNE ? bh * p.n : (bh / p.heads) * p.n;
@@ -563,8 +565,7 @@ cudaError_t launch_sd(const AttnTcArgs& a, cudaStream_t s) {
     cudaError_t err = ensure_smem_attr(kern, (int)L::kMaxSmem);
     if (err != cudaSuccess) return err;
     const unsigned grid = (unsigned)std::min<int64_t>(p.items, sm_count());
-    kern<<<grid, L::kThreads, smem_bytes, s>>>(tq, tk, tv, p);
-    return cudaGetLastError();
+    return launch_ex(kern, dim3(grid), dim3(L::kThreads), smem_bytes, s, 1, tq, tk, tv, p);
 }
 
 }  // namespace

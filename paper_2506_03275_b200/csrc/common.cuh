@@ -15,6 +15,18 @@ __device__ __forceinline__ void raise_flag(uint32_t* flags, uint32_t bit) {
     if (flags) atomicOr(flags, bit);
 }
 
+// Programmatic dependent launch (launch_util.h launch_ex): a kernel launched behind another
+// one of the block step may start its prologue (barrier init, TMEM allocation, code warm-up)
+// while the previous kernel drains.  pdl_wait() -- before the first global-memory access --
+// blocks until the previous grid has completed and its writes are visible (a no-op for a
+// plain launch); pdl_trigger() lets the NEXT kernel's CTAs be scheduled once every CTA of
+// this grid has triggered or exited.  Called after pdl_wait(), so a kernel's prologue only
+// ever overlaps its direct predecessor.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------------------
 // Exact (reference-reproducing) scalar math for CSD_MODE_CHECK.
 //

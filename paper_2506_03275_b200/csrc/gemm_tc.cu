@@ -226,6 +226,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUte
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    if (threadIdx.x == 0) pdl_trigger();
     const int ntiles = p.tiles_m * p.tiles_n;
     const int kblocks = p.k / 64;
     auto tile_mn = [&](int t, int& mt, int& nt) {
@@ -389,6 +391,8 @@ k_gemm2_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUt
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    if (threadIdx.x == 0) pdl_trigger();
     const int ntiles = p.tiles_m * p.tiles_n;  // tiles_m counts 256-row pair tiles
     const int kblocks = p.k / 64;
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
@@ -528,19 +532,7 @@ cudaError_t launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb0, const CU
     if (err != cudaSuccess) return err;
     const int tiles = p.tiles_m * p.tiles_n;
     const int grid = std::min(2 * tiles, sm_count() & ~1);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(kGemmThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, ta, tb0, tb1, tb2, p);
+    return launch_ex(kern, dim3((unsigned)grid), dim3(kGemmThreads), smem, s, 2, ta, tb0, tb1, tb2, p);
 }
 
 struct GemmShape {
@@ -562,8 +554,7 @@ cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb0, const CUt
     if (err != cudaSuccess) return err;
     const int tiles = p.tiles_m * p.tiles_n;
     const unsigned grid = (unsigned)std::min(tiles, sm_count());
-    kern<<<grid, kGemmThreads, smem, s>>>(ta, tb0, tb1, tb2, p);
-    return cudaGetLastError();
+    return launch_ex(kern, dim3(grid), dim3(kGemmThreads), smem, s, 1, ta, tb0, tb1, tb2, p);
 }
 
 // 2-D bf16 map with an explicit box (columns x rows), 128 B swizzle.

@@ -117,6 +117,10 @@ bool attn_pp_supported(const AttnTcArgs& a);
 bool attn_sd_supported(const AttnTcArgs& a);
 cudaError_t attn_sd(const AttnTcArgs& a, cudaStream_t s);
 cudaError_t attn_pp(const AttnTcArgs& a, cudaStream_t s);
+// attn_cp.cu: sparse delta attention on CTA pairs (chunk 192 / 256, E 128, with base);
+// attn_tc() dispatches to it before the ping-pong kernel (CSD_ATTN_CP=0 turns it off).
+bool attn_cp_supported(const AttnTcArgs& a);
+cudaError_t attn_cp(const AttnTcArgs& a, cudaStream_t s);
 
 // gemm_tc.cu: persistent tcgen05 GEMMs with fused epilogues (projections, dense MLP).
 // gemm_tc_enabled() is false when CSD_GEMM=cublas (A/B comparison against the library).

@@ -45,6 +45,8 @@ __global__ void __launch_bounds__(kCmThreads)
 k_chunk_means_split(const __nv_bfloat16* __restrict__ x, int64_t n, int64_t d, int64_t chunk,
                     int64_t bc_total, __nv_bfloat16* __restrict__ bop) {
     __shared__ float part[8][256];
+    pdl_wait();
+    if (threadIdx.x == 0) pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t bc = blockIdx.y;
     const int64_t col0 = (int64_t)blockIdx.x * 256 + lane * 8;
@@ -120,6 +122,8 @@ k_tile_means_tc(const __grid_constant__ CUtensorMap tm_w1, const __grid_constant
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *slot;
+    pdl_wait();
+    if (threadIdx.x == 0) pdl_trigger();
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tm_w1);
@@ -182,6 +186,8 @@ k_tile_means_tc(const __grid_constant__ CUtensorMap tm_w1, const __grid_constant
 // out = sum_k partial[k] (fixed order); with `cached`: out = |sum - cached| (mlp.cpp:116)
 __global__ void k_means_reduce(const float* __restrict__ partial, int ksplit, int64_t total,
                                const float* __restrict__ cached, float* __restrict__ out) {
+    pdl_wait();
+    if (threadIdx.x == 0) pdl_trigger();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= total) return;
     float s = partial[i];
@@ -207,7 +213,11 @@ cudaError_t prod_tile_means_tc(const void* x, const void* w1, int64_t batch, int
     __nv_bfloat16* bop = (__nv_bfloat16*)ws;
     float* partial = (float*)((char*)ws + ((2 * ntiles * 128 * d + 255) / 256) * 256);
     dim3 g1((unsigned)((d + 255) / 256), (unsigned)bc);
-    k_chunk_means_split<<<g1, kCmThreads, 0, s>>>((const __nv_bfloat16*)x, n, d, chunk, bc, bop);
+    {
+        cudaError_t e = launch_ex(k_chunk_means_split, g1, dim3(kCmThreads), 0, s, 1,
+                                  (const __nv_bfloat16*)x, n, d, chunk, bc, bop);
+        if (e != cudaSuccess) return e;
+    }
     CUtensorMap tw, tb;
     if (!make_map_bf16(&tw, w1, d, f, d, 128) || !make_map_bf16(&tb, bop, d, ntiles * 128, d, 16))
         return cudaErrorInvalidValue;
@@ -219,15 +229,19 @@ cudaError_t prod_tile_means_tc(const void* x, const void* w1, int64_t batch, int
         cudaError_t e = ensure_smem_attr(k_tile_means_tc, 227 * 1024);
         if (e != cudaSuccess) return e;
     }
-    k_tile_means_tc<<<dim3((unsigned)mtiles, (unsigned)ntiles, (unsigned)ks), 128, smem, s>>>(tw, tb, p);
+    {
+        cudaError_t e = launch_ex(k_tile_means_tc, dim3((unsigned)mtiles, (unsigned)ntiles, (unsigned)ks),
+                                  dim3(128), smem, s, 1, tw, tb, p);
+        if (e != cudaSuccess) return e;
+    }
     const int64_t total = bc * f;
     if (partials_out != nullptr) {  // the caller fuses the reduction (top-k load)
         partials_out->partial = partial;
         partials_out->ks = ks;
         return cudaGetLastError();
     }
-    k_means_reduce<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(partial, ks, total, cached, out);
-    return cudaGetLastError();
+    return launch_ex(k_means_reduce, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, s, 1,
+                     (const float*)partial, ks, total, cached, out);
 }
 
 size_t prod_means_ws_bytes(int64_t batch, int64_t n, int64_t d, int64_t f, int64_t chunk) {

@@ -155,6 +155,8 @@ k_smlp_up(const __grid_constant__ CUtensorMap tm_x, const MlpParams p) {
     uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int z = blockIdx.y, tn = blockIdx.x, TN = p.tn_width;
+    pdl_wait();  // the counts / indices come from the previous kernel (top-k)
+    if (threadIdx.x == 0) pdl_trigger();
     const int cnt = p.counts[z];
     const int n0 = tn * TN;  // first neuron slot of this tile
     const int b = z / p.chunks, c = z % p.chunks;
@@ -462,6 +464,8 @@ k_smlp_down(const __grid_constant__ CUtensorMap tm_delta, const __grid_constant_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *slot;
+    pdl_wait();
+    if (threadIdx.x == 0) pdl_trigger();
     auto kblocks_of = [&](int item) { return (p.counts[item / ntd] + 63) / 64; };
 
     if (warp == 0 || warp == 2 || warp == 3 || warp >= kXtra) {
@@ -717,14 +721,13 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
         if (e != cudaSuccess) return e;
     }
     dim3 g1((unsigned)ntiles, (unsigned)(batch * nc));
-    k_smlp_up<NT><<<g1, LU::kThreads, LU::alloc(tn_width), s>>>(tx, p);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_ex(k_smlp_up<NT>, g1, dim3(LU::kThreads), LU::alloc(tn_width), s, 1, tx, p);
     if (e != cudaSuccess) return e;
     const int sms = sm_count();
     const int64_t items = batch * nc * (d / 128);
-    k_smlp_down<NT><<<(unsigned)std::min<int64_t>(items, sms), DnLayout<NT>::kThreads,
-                      DnLayout<NT>::alloc((int)chunk), s>>>(tdl, tmc, txm, txo, p);
-    return cudaGetLastError();
+    return launch_ex(k_smlp_down<NT>, dim3((unsigned)std::min<int64_t>(items, sms)),
+                     dim3(DnLayout<NT>::kThreads), DnLayout<NT>::alloc((int)chunk), s, 1, tdl, tmc,
+                     txm, txo, p);
 }
 
 // Up-projection tiling: as many neuron tiles per chunk as fit ONE wave over the SMs

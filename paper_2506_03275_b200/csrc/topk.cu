@@ -109,6 +109,8 @@ k_topk_rows(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* __r
     __shared__ uint32_t warp_tot[2][kTopkWarps];
     __shared__ uint32_t warp_red[2][kTopkWarps];
     __shared__ uint32_t s_prefix, s_kleft;
+    pdl_wait();
+    if (threadIdx.x == 0) pdl_trigger();
 
     const int64_t row = blockIdx.x;
     const float* src = scores + row * m;
@@ -314,6 +316,8 @@ k_topk_cluster(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* 
     __shared__ uint32_t s_prefix, s_kleft, s_sel, s_shift;
     __shared__ uint32_t cta_gt[CS], warp_gt[kTopkWarps], warp_eq[kTopkWarps], cta_eq[CS];
     __shared__ uint32_t tot_bins[256];
+    pdl_wait();
+    if (threadIdx.x == 0) pdl_trigger();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t rank = cluster_rank();
     const int64_t row = blockIdx.x / CS;
@@ -551,9 +555,8 @@ cudaError_t topk_rows_fused_absdiff(const float* partial, int ks, const float* c
         cudaError_t e = ensure_smem_attr(k_topk_cluster<4, true>, 196 * 1024);
         if (e != cudaSuccess) return e;
     }
-    k_topk_cluster<4, true><<<(unsigned)(rows * 4), kTopkThreads, csm, s>>>(
-        nullptr, m, k, idx, counts, TopkFusedScores{partial, ks, cached});
-    return cudaGetLastError();
+    return launch_ex(k_topk_cluster<4, true>, dim3((unsigned)(rows * 4)), dim3(kTopkThreads), csm, s, 1,
+                     (const float*)nullptr, m, k, idx, counts, TopkFusedScores{partial, ks, cached});
 }
 
 cudaError_t topk_rows(const float* scores, int64_t rows, int64_t m, int64_t k, int32_t* idx,
@@ -567,9 +570,8 @@ cudaError_t topk_rows(const float* scores, int64_t rows, int64_t m, int64_t k, i
             cudaError_t e = ensure_smem_attr(k_topk_cluster<4, false>, 196 * 1024);
             if (e != cudaSuccess) return e;
         }
-        k_topk_cluster<4, false><<<(unsigned)(rows * 4), kTopkThreads, csm, s>>>(scores, m, k, idx, counts,
-                                                                                  TopkFusedScores{});
-        return cudaGetLastError();
+        return launch_ex(k_topk_cluster<4, false>, dim3((unsigned)(rows * 4)), dim3(kTopkThreads), csm, s,
+                         1, scores, m, k, idx, counts, TopkFusedScores{});
     }
     int p2 = 64;  // the register runs of the bitonic sort work on 64-element segments
     while (p2 < k) p2 <<= 1;
@@ -579,8 +581,8 @@ cudaError_t topk_rows(const float* scores, int64_t rows, int64_t m, int64_t k, i
         cudaError_t e = ensure_smem_attr(k_topk_rows, 196 * 1024);
         if (e != cudaSuccess) return e;
     }
-    k_topk_rows<<<(unsigned)rows, kTopkThreads, smem, s>>>(scores, m, k, idx, counts, stage, p2, sorted ? 1 : 0);
-    return cudaGetLastError();
+    return launch_ex(k_topk_rows, dim3((unsigned)rows), dim3(kTopkThreads), smem, s, 1, scores, m, k, idx,
+                     counts, stage, p2, sorted ? 1 : 0);
 }
 
 cudaError_t topk_rows_global(const float* scores, int64_t rows, int64_t m, int64_t k,
