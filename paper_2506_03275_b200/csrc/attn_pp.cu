@@ -129,7 +129,10 @@ __device__ __forceinline__ uint64_t pp_globaltimer() {
 
 // kPoly > 0: every kPoly-th exponential pair of a row runs as a degree-3 polynomial on the
 // FMA pipe instead of MUFU (ex2_poly2), balancing the two pipes.
-template <int E, int kPoly>
+// kOrd: the launch carries an LPT item order (p.order).  Without it the order indirection is
+// compiled out: a kernel-wide order pointer is otherwise spilled (128-register launch bound)
+// and reloaded from local memory at every item lookup.
+template <int E, int kPoly, bool kOrd>
 __global__ void __launch_bounds__(PPLayout<E>::kThreads, 1)
 k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
           const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_b,
@@ -185,11 +188,13 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     }
     // work positions -> items: longest-first order for ragged index sets (p.order, LPT), or
     // the identity; every role walks POSITIONS pos = blockIdx.x + i * gridDim.x
-    const int32_t* order = (p.order != nullptr && p.order[items] == 0) ? p.order : nullptr;
-    auto item_at = [&](int pos) -> int { return order != nullptr ? order[pos] : pos; };
-    auto count_of = [&](int pos) -> int { return dense ? p.n : p.counts[item_at(pos)]; };
+    const int32_t* order = (kOrd && p.order[items] == 0) ? p.order : nullptr;
+    // (captured by value: a by-reference capture gives `order` a stack slot that every
+    // asm "memory" clobber then reloads -- LDL on the hot paths)
+    auto item_at = [order](int pos) -> int { return order != nullptr ? order[pos] : pos; };
+    auto count_of = [=](int pos) -> int { return dense ? p.n : p.counts[item_at(pos)]; };
     // next live (count > 0) item of this CTA at or after `from`
-    auto next_live = [&](int from, int& cnt_out) -> int {
+    auto next_live = [=](int from, int& cnt_out) -> int {
         int x = from;
         cnt_out = 0;
         for (; x < items; x += gridDim.x) {
@@ -198,7 +203,7 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
         }
         return x;
     };
-    auto item_rows = [&](int pos, int& row_base, int& col0) {
+    auto item_rows = [=](int pos, int& row_base, int& col0) {
         const int it = item_at(pos);
         const int bh = it / p.chunks;
         row_base = p.layout == CSD_LAYOUT_BHNE ? bh * p.n : (bh / p.heads) * p.n;
@@ -212,7 +217,7 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     constexpr int kRowStep = L::kCopyThreads / (E / 8);
     constexpr int kCpRows = (128 + kRowStep - 1) / kRowStep;
     const int cp_thread = warp < 4 ? (warp - 2) * 32 + lane : 64 + (warp - 12) * 32 + lane;
-    auto load_ids = [&](int it, int cnt, int j, int32_t (&id)[kCpRows]) {
+    auto load_ids = [=](int it, int cnt, int j, int32_t (&id)[kCpRows]) {
         const int r0 = cp_thread / (E / 8);
         const int32_t* ids = p.idx + (int64_t)(it < items ? item_at(it) : 0) * p.k_max;
 #pragma unroll
@@ -685,25 +690,28 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                     for (int oc = 0; oc < E / 32; ++oc)
                         tmem_ld32(tO + oc * 32, *reinterpret_cast<uint32_t(*)[32]>(&ro[oc * 32]));
                     tmem_ld_wait();
+                    // per 64-column strip: the row's 8 base pieces loaded together, then
+                    // combined and stored (independent loads in flight, not a load-use chain)
 #pragma unroll
-                    for (int oc = 0; oc < E / 32; ++oc) {
-                        const uint32_t* r = ro + oc * 32;
+                    for (int hf = 0; hf < E / 64; ++hf) {
                         if (!row_ok) continue;
-                        uint8_t* rowp = sx + (oc >> 1) * p.x_strip + crow * 128;
+                        uint8_t* rowp = sx + hf * p.x_strip + crow * 128;
+                        uint4 bv[8];
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const int cidx = (oc & 1) * 4 + q;
-                            uint4* ptr = reinterpret_cast<uint4*>(rowp + ((cidx ^ (crow & 7)) << 4));
-                            const uint4 bv = *ptr;
-                            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bv);
+                        for (int q = 0; q < 8; ++q)
+                            bv[q] = *reinterpret_cast<const uint4*>(rowp + ((q ^ (crow & 7)) << 4));
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bv[q]);
+                            const uint32_t* r = ro + hf * 64 + q * 8;
                             uint32_t o4[4];
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
                                 const float2 f = __bfloat1622float2(b2[u]);
-                                o4[u] = pack_bf16x2(fmaf(fsc, __uint_as_float(r[q * 8 + 2 * u]), f.x),
-                                                    fmaf(fsc, __uint_as_float(r[q * 8 + 2 * u + 1]), f.y));
+                                o4[u] = pack_bf16x2(fmaf(fsc, __uint_as_float(r[2 * u]), f.x),
+                                                    fmaf(fsc, __uint_as_float(r[2 * u + 1]), f.y));
                             }
-                            st_shared_v4_if(!dry, ptr, o4);  // dry pass: no store
+                            st_shared_v4_if(!dry, rowp + ((q ^ (crow & 7)) << 4), o4);  // dry pass: no store
                         }
                     }
                     fence_proxy_async_smem();  // in-place writes -> async proxy (TMA store)
@@ -850,8 +858,8 @@ cudaError_t launch_pp(const AttnTcArgs& a, cudaStream_t s) {
         return e ? std::atoi(e) : -1;
     }();
     const int poly = poly_env >= 0 ? poly_env : (a.idx == nullptr ? 4 : 0);
-    auto kern = poly == 4 ? k_attn_pp<E, 4> : poly == 3 ? k_attn_pp<E, 3> : poly == 2 ? k_attn_pp<E, 2>
-                                                                                    : k_attn_pp<E, 0>;
+    auto kern = a.order != nullptr ? (poly == 4 ? k_attn_pp<E, 4, true> : k_attn_pp<E, 0, true>)
+                                   : (poly == 4 ? k_attn_pp<E, 4, false> : k_attn_pp<E, 0, false>);
     cudaError_t err = ensure_smem_attr(kern, (int)L::kMaxSmem);
     if (err != cudaSuccess) return err;
     const unsigned grid = (unsigned)std::min<int64_t>(p.items, sm_count());
