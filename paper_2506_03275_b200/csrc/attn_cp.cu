@@ -699,7 +699,7 @@ cudaError_t attn_cp(const AttnTcArgs& a, cudaStream_t s) {
     cudaError_t err = ensure_smem_attr(kern, (int)kMaxSmem);
     if (err != cudaSuccess) return err;
     const int npairs = (int)std::min<int64_t>(p.items, sm_count() / 2);
-    return launch_ex(kern, dim3(2u * (unsigned)npairs), dim3(kThreads), smem_bytes, s, 2, tq, tb, to, p);
+    return launch_ex_pdl(1, kern, dim3(2u * (unsigned)npairs), dim3(kThreads), smem_bytes, s, 2, tq, tb, to, p);
 }
 
 }  // namespace dev

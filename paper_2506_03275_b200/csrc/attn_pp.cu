@@ -863,7 +863,7 @@ cudaError_t launch_pp(const AttnTcArgs& a, cudaStream_t s) {
     cudaError_t err = ensure_smem_attr(kern, (int)L::kMaxSmem);
     if (err != cudaSuccess) return err;
     const unsigned grid = (unsigned)std::min<int64_t>(p.items, sm_count());
-    return launch_ex(kern, dim3(grid), dim3(L::kThreads), smem_bytes, s, 1, tq, tk, tv, tb, to, p);
+    return launch_ex_pdl(1, kern, dim3(grid), dim3(L::kThreads), smem_bytes, s, 1, tq, tk, tv, tb, to, p);
 }
 
 }  // namespace

@@ -61,20 +61,24 @@ inline int sm_count() {
 // graph replays): the kernels start 12-40 us early but the sparse step ends at the same time
 // (425 vs 428 us) -- every kernel's main work depends on its predecessor's output and the
 // persistent grids take statically assigned work, so only prologues overlap.
-inline bool pdl_enabled() {
-    static const bool on = [] {
+// CSD_PDL=1: only the launches that profit (the attention kernels behind the Q/K/V GEMM:
+// their code warm-up and barrier / TMEM setup overlap the GEMM's tail); CSD_PDL=2: every
+// block-step kernel.
+inline int pdl_mode() {
+    static const int m = [] {
         const char* e = std::getenv("CSD_PDL");
-        return e != nullptr && std::atoi(e) != 0;
+        return e != nullptr ? std::atoi(e) : 0;
     }();
-    return on;
+    return m;
 }
+inline bool pdl_enabled(int level = 2) { return pdl_mode() >= level; }
 
 // cudaLaunchKernelEx with the programmatic-serialization attribute (when enabled) and an
 // optional cluster shape (cluster_x > 1).  Every kernel launched through here calls
 // pdl_wait() before its first global-memory access.
 template <typename... KArgs, typename... Args>
-inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                             cudaStream_t s, unsigned cluster_x, Args&&... args) {
+inline cudaError_t launch_ex_pdl(int pdl_level, void (*kern)(KArgs...), dim3 grid, dim3 block,
+                                 size_t smem, cudaStream_t s, unsigned cluster_x, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -82,7 +86,7 @@ inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
     int na = 0;
-    if (pdl_enabled()) {
+    if (pdl_enabled(pdl_level)) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
@@ -97,6 +101,11 @@ inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size
     cfg.attrs = attr;
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t s, unsigned cluster_x, Args&&... args) {
+    return launch_ex_pdl(2, kern, grid, block, smem, s, cluster_x, std::forward<Args>(args)...);
 }
 
 }  // namespace dev
