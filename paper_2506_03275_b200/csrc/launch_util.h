@@ -57,10 +57,14 @@ inline int sm_count() {
 }
 
 // Programmatic dependent launch for the block-step kernels (common.cuh pdl_wait /
-// pdl_trigger), opt-in with CSD_PDL=1.  Measured on the FLUX block (r02, CUPTI timeline of
-// graph replays): the kernels start 12-40 us early but the sparse step ends at the same time
-// (425 vs 428 us) -- every kernel's main work depends on its predecessor's output and the
-// persistent grids take statically assigned work, so only prologues overlap.
+// pdl_trigger).  Measured on the FLUX block (r02, CUPTI timeline of graph replays): with
+// every kernel behind its predecessor (CSD_PDL=2) the kernels start 12-40 us early but the
+// sparse step ends at the same time (425 vs 428 us) -- every kernel's main work depends on
+// its predecessor's output and the persistent grids take statically assigned work, so only
+// prologues overlap; with the attention kernels alone (CSD_PDL=1: their barrier / TMEM
+// setup and dead-warp code warm-up overlap the Q/K/V GEMM's tail) the sparse step measured
+// 409.2 -> 405.9 us on one box and 413.4 -> 414.9 us on another: within noise, so it stays
+// opt-in (default 0).
 // CSD_PDL=1: only the launches that profit (the attention kernels behind the Q/K/V GEMM:
 // their code warm-up and barrier / TMEM setup overlap the GEMM's tail); CSD_PDL=2: every
 // block-step kernel.
