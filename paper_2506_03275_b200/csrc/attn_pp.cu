@@ -581,6 +581,7 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                     continue;
                 }
                 const bool wait = live && !dry;
+                if (threadIdx.x == 128 * (t + 1)) PP_TRACE(22 + t, li);  // item set up
                 const uint32_t tP = dry ? tO : tS;  // P destination
                 const int nblk = (cnt + 127) / 128;
                 float m_run = -INFINITY, m_true = -INFINITY, l_run = 0.f;

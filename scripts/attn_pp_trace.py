@@ -92,6 +92,7 @@ def main():
         print("  Q issue t0/t1 per item:", " ".join(f"{kc(13, li)}/{kc(14, li)}" for li in range(6)))
         print("  epilogue t0 [start end] per item:",
               " ".join(f"[{kc(11, 2 * li)} {kc(11, 2 * li + 1)}]" for li in range(6)))
+        print("  item set-up t0 / t1:", " ".join(f"{kc(22, li)}/{kc(23, li)}" for li in range(6)))
         print("  epilogue t1 [start end] per item:",
               " ".join(f"[{kc(12, 2 * li)} {kc(12, 2 * li + 1)}]" for li in range(6)))
         print("    g " + " ".join(f"{n:>6s}" for n in EV) + " " + " ".join(f"{n:>6s}" for _, n in EV2))
