@@ -55,7 +55,7 @@ k_chunk_means_split(const __nv_bfloat16* __restrict__ x, int64_t n, int64_t d, i
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (col0 < d) {
         const __nv_bfloat16* src = x + (b * n + c * chunk) * d + col0;
-#pragma unroll 12
+#pragma unroll 24
         for (int64_t r = warp; r < chunk; r += 8) {
             const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + r * d));
             const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
