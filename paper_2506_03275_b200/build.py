@@ -32,6 +32,7 @@ PER_FILE = {
     # predicated stamps cost 4 us of instruction fetch in the CTA-pair attention kernel
     "attn_cp.cu": [] if os.environ.get("CSD_TRACE") else ["-DCSD_CP_NOTRACE"],
     "attn_pp.cu": [] if os.environ.get("CSD_TRACE") else ["-DCSD_PP_NOTRACE"],
+    "attn_sd.cu": [] if os.environ.get("CSD_TRACE") else ["-DCSD_SD_NOTRACE"],
     "check_kernels.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false"],
     # the CHECK latent update is the reference's separate multiply and add
     "generation.cu": ["-fmad=false"],

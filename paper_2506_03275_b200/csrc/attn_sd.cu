@@ -81,11 +81,17 @@ struct SDParams {
     uint64_t* trace;  // debug timeline (null: off), 8 CTAs x 2048 clock64 stamps
 };
 
+#ifdef CSD_SD_NOTRACE  // production builds (paper_2506_03275_b200/build.py; CSD_TRACE=1 keeps it)
+#define SD_TRACE(ev, ix) \
+    do {                 \
+    } while (0)
+#else
 #define SD_TRACE(ev, ix)                                                                     \
     do {                                                                                     \
         if (p.trace != nullptr && blockIdx.x < 8)                                            \
             p.trace[blockIdx.x * 2048 + (ev) * 64 + ((ix) & 63)] = clock64();                \
     } while (0)
+#endif
 
 __device__ __forceinline__ int64_t sd_tok_off(int layout, int64_t b, int64_t h, int64_t tok,
                                               int heads, int n, int e) {
@@ -185,7 +191,7 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                         for (int bx = 0; bx < 2; ++bx) tma_prefetch_2d(&tm_q, ncol0 + hf * 64, nqr + bx * 64);
                 }
             }
-        } else if (warp == 0 && lane == 1) {
+        } else if (warp == 2 && lane == 0) {  // own warp: a divergent lane of warp 0 waits behind the Q loader's spins
             // ---------------------------------------------------------- K / V TMA tiles
             tma_prefetch_desc(&tm_k);
             tma_prefetch_desc(&tm_v);
