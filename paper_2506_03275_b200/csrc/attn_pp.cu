@@ -20,9 +20,11 @@
 // TMEM (512 columns): S_0 [0,128), S_1 [128,256) (P_t aliased over the first 64 columns of
 // S_t as bf16 pairs), O_0 [256, 256+E), O_1 [256+E, 256+2E).
 //
-// Roles (16 warps): warp 0 lane 0 Q loader, lane 1 dense K/V TMA loader, lane 31 staged-base
-// I/O; warp 1 MMA issuer; warps 2-3 and 12-15 sparse K/V row copies (cp.async); warps 4-7
-// softmax tile 0; warps 8-11 softmax tile 1.
+// Roles (16 warps): warp 0 lane 0 Q loader; warp 1 MMA issuer; warp 2 lane 0 dense K/V TMA
+// loader (dense passes) or, with warps 12-15, the sparse K/V row copies (cp.async); warp 3
+// lane 0 staged-base / out I/O; warps 4-7 softmax tile 0; warps 8-11 softmax tile 1.  (Each
+// single-thread role has its own warp: divergent lanes of one warp delay each other's
+// barrier waits.)
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -56,7 +58,7 @@ struct PPLayout {
     static constexpr uint32_t kStrip = 128 * 128;      // 128 rows x 128 B
     static constexpr uint32_t kKV = kHalves * kStrip;  // one K or V block
     static constexpr uint32_t kThreads = 512;
-    static constexpr int kCopyThreads = 192;  // warps 2, 3, 12-15
+    static constexpr int kCopyThreads = 160;  // warps 2, 12-15 (warp 3: staged base / out I/O)
     static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kOcol = 256;    // O_0 column
     static constexpr uint32_t kMaxSmem = 227 * 1024;
@@ -216,7 +218,7 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     static_assert(L::kCopyThreads % (E / 8) == 0, "copy threads per row");
     constexpr int kRowStep = L::kCopyThreads / (E / 8);
     constexpr int kCpRows = (128 + kRowStep - 1) / kRowStep;
-    const int cp_thread = warp < 4 ? (warp - 2) * 32 + lane : 64 + (warp - 12) * 32 + lane;
+    const int cp_thread = warp == 2 ? lane : 32 + (warp - 12) * 32 + lane;
     auto load_ids = [=](int it, int cnt, int j, int32_t (&id)[kCpRows]) {
         const int r0 = cp_thread / (E / 8);
         const int32_t* ids = p.idx + (int64_t)(it < items ? item_at(it) : 0) * p.k_max;
@@ -228,7 +230,7 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     };
     int cp_it = items, cp_cnt = 0;
     int32_t cp_id[kCpRows];
-    if (cpa && (warp == 2 || warp == 3 || warp >= 12)) {
+    if (cpa && (warp == 2 || warp >= 12)) {
         pdl_wait();  // the counts / indices may come from the previous kernel (dense step top-k)
         cp_it = next_live(blockIdx.x, cp_cnt);
         load_ids(cp_it, cp_cnt, 0, cp_id);
@@ -273,7 +275,9 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                     }
                     it = nx;
                 }
-            } else if (lane == 1 && dense) {
+            }
+        } else if (warp == 2 && dense) {  // own warp (a divergent lane of warp 0 waits behind its spins)
+            if (lane == 0) {
                 // ---------------------------------------------------- dense K/V TMA tiles
                 tma_prefetch_desc(&tm_k);
                 tma_prefetch_desc(&tm_v);
@@ -298,7 +302,9 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                                         col0 + hf * 64, kr0 + j * 128);
                     }
                 }
-            } else if (lane == 31 && p.stage_base) {
+            }
+        } else if (warp == 3) {
+            if (lane == 0 && p.stage_base) {
                 // ---------------------------------------------------- staged base / out I/O
                 const int nbox = (p.chunk + 63) >> 6;
                 auto issue_base = [&](int it) {
