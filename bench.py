@@ -381,15 +381,17 @@ def run_ours(args, rank, world):
                                 "profiles/latest_full.json)",
                 "alg_bytes": att["alg_bytes"],
                 "tensor_frac": round(att["flops"] / (att["ms"] * 1e-3) / 1e12 / tf, 4),
-                # the K/V rows gathered by cp.async from 6 copy warps (LSU path, 36-40 B/ns per
+                # the K/V rows gathered by cp.async from 5 copy warps (LSU path, 36-40 B/ns per
                 # SM L2-resident, scripts/gather_bench2.cu); not the binding resource either
                 "gather": {"bytes": att["gather_bytes"],
                            "achieved_gbs": round(att["gather_bytes"] / (att["ms"] * 1e-3) / 1e9, 1),
                            "measured_cp_async_gbs": 148 * 40.0,
                            "frac": round(att["gather_bytes"] / (att["ms"] * 1e-3) / 1e9 / (148 * 40.0), 4)},
-                "limiter": "per-item latency: ~4 items of 3 key blocks per SM, each block a "
-                           "MUFU-bound softmax (2.3k cycles) -> P.V -> next S chain plus the item "
-                           "epilogue (scripts/attn_pp_trace.py timelines, DESIGN.md 4.3)",
+                "limiter": "per-item latency: ~4 items of 3 key blocks per SM; per block the "
+                           "softmax of one warp per row quadrant (2.0-2.3k cycles, bound by the "
+                           "warp's own MUFU issue rate) -> P.V -> next S chain (~4.4k cycles), "
+                           "plus the item epilogue and a cold first item after the Q/K/V GEMM "
+                           "(scripts/attn_pp_trace.py timelines, DESIGN.md 4.1-4.3)",
             },
         }
     return out
