@@ -295,6 +295,15 @@ csd_status csd_block_rows_step(csd_block* blk, const void* x_rows, const void* a
 /* out_bf16 = bf16(x_bf16 + partial_f32) (PROD residual after an all-reduce). */
 csd_status csd_residual_add(csd_ctx* ctx, const void* x, const float* partial, int64_t numel,
                             void* out, void* stream);
+/* Cache arena (memory.cpp:33-58): a block's persistent caches -- attention residual, softmax
+ * stats, index sets, MLP activations / outputs / tile means -- live in one device
+ * allocation.  csd_block_cache_arena reports it; csd_block_bind_cache_arena re-points the
+ * caches into caller storage of at least that size (same layout, contents not copied; the
+ * block's own arena is freed), so a layer stack can keep two arenas on the device and stream
+ * the rest to host memory (generation.Generation(offload=True)). */
+csd_status csd_block_cache_arena(csd_block* blk, void** dev_ptr, size_t* bytes);
+csd_status csd_block_bind_cache_arena(csd_block* blk, void* dev_ptr, size_t bytes);
+
 /* Cache views (reference layouts, fp32, device): which = 0 attn residual
  * [B,H,N,E], 1 row_max, 2 exp_sum [B,H,N], 3 mlp act [B,N,F], 4 mlp out
  * [B,N,D], 5 tile means [B,C,F]; 6/7 attention / mlp index sets (int32). */

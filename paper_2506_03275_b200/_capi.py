@@ -70,6 +70,8 @@ SIGNATURES = {
     "csd_block_create": (i32, [p, i32, C.POINTER(BlockConfig)] + [fp] * 8 + [C.POINTER(p)]),
     "csd_block_destroy": (i32, [p]),
     "csd_block_reset": (i32, [p]),
+    "csd_block_cache_arena": (i32, [p, C.POINTER(p), C.POINTER(C.c_size_t)]),
+    "csd_block_bind_cache_arena": (i32, [p, p, C.c_size_t]),
     "csd_block_step": (i32, [p, fp, fp, C.c_int, fp, fp, i64, p]),
     "csd_block_cache": (i32, [p, C.c_int, fp, fp, p]),
     "csd_block_attn_partial": (i32, [p, fp, C.c_int, fp, p]),

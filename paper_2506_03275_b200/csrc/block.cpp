@@ -60,14 +60,43 @@ struct csd_block {
     int64_t mB = 0, mN = 0;
     bool token_mode = false;
 
+    // The persistent caches (everything a later step reads: attention residual, stats, index
+    // sets, MLP activations / outputs / tile means) live in ONE arena, so a layer stack can
+    // keep two arenas on the device and stream the others to host memory (memory.cpp:33-58,
+    // "optimized double-buffers two layers while the rest live off-device";
+    // csd_block_bind_cache_arena).  Per-step scratch stays in `allocs`.
+    void* arena = nullptr;
+    bool arena_owned = true;
+    size_t arena_bytes = 0;
+    std::vector<std::pair<void**, size_t>> arena_slots;  // (pointer field, offset)
+
     void* alloc(size_t bytes) {
         void* p = nullptr;
         if (cudaMalloc(&p, bytes < 256 ? 256 : bytes) != cudaSuccess) return nullptr;
         allocs.push_back(p);
         return p;
     }
+    // reserve `bytes` of the cache arena for *field (bound by finish_arena)
+    void cache_alloc(void** field, size_t bytes) {
+        arena_slots.emplace_back(field, arena_bytes);
+        arena_bytes += (bytes + 255) & ~size_t(255);
+    }
+    bool bind_arena(void* base) {
+        for (auto& sl : arena_slots) *sl.first = static_cast<char*>(base) + sl.second;
+        arena = base;
+        return true;
+    }
+    bool finish_arena() {
+        if (cudaMalloc(&arena, arena_bytes < 256 ? 256 : arena_bytes) != cudaSuccess) {
+            arena = nullptr;
+            return false;
+        }
+        arena_owned = true;
+        return bind_arena(arena);
+    }
     ~csd_block() {
         for (void* p : allocs) cudaFree(p);
+        if (arena_owned && arena) cudaFree(arena);
     }
 };
 
@@ -172,31 +201,33 @@ csd_status csd_block_create(csd_ctx* ctx, csd_mode mode, const csd_block_config*
     blk->mN = token_mode ? c.t_local : N;
     const int64_t MR = blk->mB * blk->mN, MC = MR / c.chunk;  // MLP rows / chunks
     const size_t es = esz(mode);
+    // per-step scratch
     blk->q = blk->alloc(es * B * N * Dl);
     blk->k = blk->alloc(es * B * N * Dl);
     blk->v = blk->alloc(es * B * N * Dl);
     blk->attn = blk->alloc(es * B * N * Dl);
-    blk->resid = blk->alloc(es * B * N * Dl);
     blk->x_mid = blk->alloc(es * (token_mode ? MR : B * N) * D);
     blk->proj = (float*)blk->alloc(4 * B * N * D);
-    for (int i = 0; i < 2; ++i) {
-        blk->m[i] = (float*)blk->alloc(4 * B * Hl * N);
-        blk->l[i] = (float*)blk->alloc(4 * B * Hl * N);
-    }
     blk->colsum = (float*)blk->alloc(4 * B * Hl * C * N);
+    // persistent caches: one arena
     const int64_t ak = c.attn_k > 0 ? c.attn_k : N;
-    blk->a_kmax = ak;
-    blk->aidx = (int32_t*)blk->alloc(4 * B * Hl * C * ak);
-    blk->acnt = (int32_t*)blk->alloc(4 * B * Hl * C);
-    blk->tmeans = (float*)blk->alloc(4 * MC * Fl);
-    blk->act = blk->alloc(es * MR * Fl);
-    blk->mout = (float*)blk->alloc(4 * MR * D);
     const int64_t mk = c.mlp_k > 0 ? c.mlp_k : Fl;
-    blk->midx = (int32_t*)blk->alloc(4 * MC * mk);
-    blk->mcnt = (int32_t*)blk->alloc(4 * MC);
-    (void)C;
+    blk->a_kmax = ak;
+    blk->cache_alloc(&blk->resid, es * B * N * Dl);
+    for (int i = 0; i < 2; ++i) {
+        blk->cache_alloc(reinterpret_cast<void**>(&blk->m[i]), 4 * B * Hl * N);
+        blk->cache_alloc(reinterpret_cast<void**>(&blk->l[i]), 4 * B * Hl * N);
+    }
+    blk->cache_alloc(reinterpret_cast<void**>(&blk->aidx), 4 * B * Hl * C * ak);
+    blk->cache_alloc(reinterpret_cast<void**>(&blk->acnt), 4 * B * Hl * C);
+    blk->cache_alloc(reinterpret_cast<void**>(&blk->tmeans), 4 * MC * Fl);
+    blk->cache_alloc(&blk->act, es * MR * Fl);
+    blk->cache_alloc(reinterpret_cast<void**>(&blk->mout), 4 * MR * D);
+    blk->cache_alloc(reinterpret_cast<void**>(&blk->midx), 4 * MC * mk);
+    blk->cache_alloc(reinterpret_cast<void**>(&blk->mcnt), 4 * MC);
     for (void* p : blk->allocs)
         if (!p) return fail(set_error(CSD_ERR_CUDA, "block allocation failed"));
+    if (!blk->finish_arena()) return fail(set_error(CSD_ERR_CUDA, "block cache arena allocation failed"));
     *out = blk;
     return CSD_OK;
 }
@@ -208,6 +239,32 @@ csd_status csd_block_reset(csd_block* blk) {
     blk->attn_init = blk->mlp_init = false;
     blk->attn_age = blk->mlp_age = 0;
     blk->cur = 0;
+    return CSD_OK;
+}
+
+csd_status csd_block_cache_arena(csd_block* blk, void** dev_ptr, size_t* bytes) {
+    if (!blk) return set_error(CSD_ERR_VALUE, "null block");
+    if (dev_ptr) *dev_ptr = blk->arena;
+    if (bytes) *bytes = blk->arena_bytes;
+    return CSD_OK;
+}
+
+csd_status csd_block_bind_cache_arena(csd_block* blk, void* dev_ptr, size_t bytes) {
+    // Re-point the block's caches into caller storage of >= csd_block_cache_arena bytes (the
+    // same layout); the block's own arena is released.  The contents are NOT copied: the caller
+    // moves them (a layer stack streams each layer's arena between host memory and two device
+    // slots).  CUDA graphs captured before a rebind keep the old addresses.
+    if (!blk || !dev_ptr) return set_error(CSD_ERR_VALUE, "null block or arena");
+    if (bytes < blk->arena_bytes)
+        return set_error(CSD_ERR_SHAPE, "cache arena of %zu bytes < the block's %zu", bytes, blk->arena_bytes);
+    if (reinterpret_cast<uintptr_t>(dev_ptr) % 256 != 0)
+        return set_error(CSD_ERR_VALUE, "cache arena must be 256-byte aligned");
+    if (blk->arena_owned && blk->arena && blk->arena != dev_ptr) {
+        cudaDeviceSynchronize();
+        cudaFree(blk->arena);
+    }
+    blk->arena_owned = false;
+    blk->bind_arena(dev_ptr);
     return CSD_OK;
 }
 

@@ -12,6 +12,13 @@ Device residency: the fp32 master latent, its bf16 shadow (PROD block input), th
 layer outputs and the block caches stay in HBM for the whole run; in PROD each step
 kind (dense / sparse / skipped) is one CUDA graph replay.  Nothing here computes on
 the CPU except the schedule (a few integers).
+
+Cache offload (``offload=True``, memory.cpp:33-58 "optimized double-buffers two layers while
+the rest live off-device"): every layer's persistent caches are one arena
+(csd_block_bind_cache_arena); two device arenas serve the whole stack (layer l uses slot
+l % 2) and the others live in pinned host memory.  While layer l computes, the previous user
+of the other slot is copied out on one copy stream and the next layer's arena copied in on
+another, so the device holds 2 / L of the caches (plus one layer's per-step scratch each).
 """
 from __future__ import annotations
 
@@ -101,7 +108,8 @@ class Generation:
     measured against (model_forward_dense per step); None skips the R^2 report."""
 
     def __init__(self, layers: List[ops.Block], layout: ops.VoxelLayout,
-                 baseline: Optional[List[ops.Block]] = None, use_graphs: Optional[bool] = None):
+                 baseline: Optional[List[ops.Block]] = None, use_graphs: Optional[bool] = None,
+                 offload: bool = False):
         if not layers:
             raise ValueError("a generation needs at least one layer")
         self.layers = layers
@@ -123,15 +131,83 @@ class Generation:
         self.shadow = torch.empty(self.shape, dtype=torch.bfloat16, device=dev) if self.prod else None
         self.outs = [torch.empty(self.shape, dtype=dt, device=dev) for _ in layers]
         self._graphs = {}
+        self.offload = bool(offload) and len(layers) > 2
+        if self.offload:
+            nbytes = max(blk.cache_arena()[1] for blk in layers)
+            self._slots = [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
+            self._host = []
+            for l, blk in enumerate(layers):
+                blk.bind_cache_arena(self._slots[l % 2])
+                self._host.append(torch.zeros(nbytes, dtype=torch.uint8, pin_memory=True))
+            self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+            self._ready = [None] * len(layers)  # H2D of layer l's arena into its slot done
+            self.arena_bytes = nbytes
+
+    def memory_report(self) -> dict:
+        """Cache bytes on the device, resident vs offloaded (memory.cpp:47-53 act_naive /
+        act_resident, here measured from the arenas)."""
+        n = max(blk.cache_arena()[1] for blk in self.layers)
+        resident = (2 if self.offload else len(self.layers)) * n
+        return {"arena_bytes_per_layer": n, "layers": len(self.layers),
+                "cache_naive_bytes": len(self.layers) * n, "cache_device_bytes": resident,
+                "cache_host_bytes": len(self.layers) * n if self.offload else 0}
+
+    def _next_user(self, l: int) -> int:
+        """The layer that uses slot l % 2 next after layer l (the stack repeats every step)."""
+        L = len(self.layers)
+        for k in range(1, L + 1):
+            m = (l + k) % L
+            if m % 2 == l % 2:
+                return m
+        return l
+
+    def _prefetch(self, l: int, after=None):
+        """H2D of layer l's arena into its slot on the copy stream (after `after`)."""
+        with torch.cuda.stream(self._h2d):
+            if after is not None:
+                self._h2d.wait_event(after)
+            self._slots[l % 2].copy_(self._host[l], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self._h2d)
+            self._ready[l] = ev
 
     def _input(self):
         return self.shadow if self.prod else self.latent
 
     def _forward(self, dense: bool):
         cur = self._input()
-        for blk, out in zip(self.layers, self.outs):
+        if not self.offload:
+            for blk, out in zip(self.layers, self.outs):
+                blk.step(cur, dense, out=out)
+                cur = out
+            return
+        stream = torch.cuda.current_stream()
+        L = len(self.layers)
+        # the first two layers' arenas come in before the stack starts (a step's last copies
+        # are joined below, so every step -- and every captured graph -- is self-contained)
+        for l in range(min(2, L)):
+            self._prefetch(l, after=self._mark(stream))
+        for l, (blk, out) in enumerate(zip(self.layers, self.outs)):
+            stream.wait_event(self._ready[l])
             blk.step(cur, dense, out=out)
             cur = out
+            done = self._mark(stream)
+            with torch.cuda.stream(self._d2h):  # this layer's caches back to host memory
+                self._d2h.wait_event(done)
+                self._host[l].copy_(self._slots[l % 2], non_blocking=True)
+                saved = torch.cuda.Event()
+                saved.record(self._d2h)
+            n = self._next_user(l)
+            if n > l:  # a later layer of this step reuses the slot
+                self._prefetch(n, after=saved)
+        stream.wait_stream(self._d2h)
+        stream.wait_stream(self._h2d)
+
+    @staticmethod
+    def _mark(stream):
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        return ev
 
     def _step(self, mode: int, scale: float):
         if mode != SKIPPED:

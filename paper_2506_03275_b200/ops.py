@@ -553,6 +553,21 @@ class Block:
         """A fresh ModelState for this layer (model.cpp:101-105): the next step must be dense."""
         raise_for(self.ctx.lib, self.ctx.lib.csd_block_reset(self.h))
 
+    def cache_arena(self):
+        """(device pointer, bytes) of the one allocation holding this layer's persistent caches."""
+        ptr, n = C.c_void_p(), C.c_size_t()
+        raise_for(self.ctx.lib, self.ctx.lib.csd_block_cache_arena(self.h, C.byref(ptr), C.byref(n)))
+        return ptr.value, n.value
+
+    def bind_cache_arena(self, storage: torch.Tensor):
+        """Re-point this layer's caches into `storage` (a device uint8 tensor of at least
+        cache_arena() bytes, same layout; contents not copied).  The block keeps a reference."""
+        if not storage.is_cuda or storage.dtype != torch.uint8:
+            raise TypeError("cache storage is a device uint8 tensor")
+        raise_for(self.ctx.lib, self.ctx.lib.csd_block_bind_cache_arena(
+            self.h, C.c_void_p(storage.data_ptr()), storage.numel()))
+        self._arena_storage = storage
+
     def attn_heads(self, x: torch.Tensor, dense: bool, out: Optional[torch.Tensor] = None):
         """Token-sharded step, part 1: this block's heads over every token -> [B*N, Dl] bf16."""
         c = self.cfg

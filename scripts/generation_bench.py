@@ -26,6 +26,9 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--layers", type=int, default=1)
     ap.add_argument("--no-r2", action="store_true")
+    ap.add_argument("--offload", action="store_true",
+                    help="also run the chipmunk schedule with two layers' caches on the device and "
+                         "the rest streamed from pinned host memory (Generation(offload=True))")
     args = ap.parse_args()
     cfg = dict(bench.FLUX)
     t, h, w = cfg["grid"]
@@ -39,18 +42,25 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(1235)
     grid0 = torch.randn((1, t, h, w, cfg["dim"]), device="cuda", generator=g)
     rows = {}
-    for name, sched in (("dense", G.ScheduleParams(args.steps, 0)),
-                        ("chipmunk", G.ScheduleParams(args.steps, 10, True, min(30, args.steps), 4))):
+    chip = G.ScheduleParams(args.steps, 10, True, min(30, args.steps), 4)
+    runs = [("dense", G.ScheduleParams(args.steps, 0), False), ("chipmunk", chip, False)]
+    if args.offload:
+        runs.append(("chipmunk_offload", chip, True))
+    finals = {}
+    for name, sched, off in runs:
         layers = [ops.Block(bc, wt, production=True) for wt in weights]
         base = None
         if name == "chipmunk" and not args.no_r2:
             base = [ops.Block(bc, wt, production=True) for wt in weights]
-        gen = G.Generation(layers, layout, baseline=base)
+        gen = G.Generation(layers, layout, baseline=base, offload=off)
         gen.run(grid0, sched)  # warm (graph capture, workspaces)
         rep = gen.run(grid0, sched)
+        finals[name] = rep.final_latent
         rows[name] = {"device_ms": round(rep.device_ms, 3),
                       "modes": {G.MODE_NAMES[m]: rep.modes.count(m) for m in (0, 1, 2)},
-                      "end_to_end_r2": rep.end_to_end_r2}
+                      "end_to_end_r2": rep.end_to_end_r2, "memory": gen.memory_report()}
+        if off:
+            rows[name]["bit_identical_to_resident"] = bool(torch.equal(finals[name], finals["chipmunk"]))
         for blk in layers + (base or []):
             blk.close()
         torch.cuda.empty_cache()

@@ -125,3 +125,38 @@ def test_r_squared_matches_definition(cuda):
     assert abs(got - want) < 1e-10
     with pytest.raises(errors.NumericError):
         G.r_squared(o, a, o)  # zero-variance true delta
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("layers,prod", [(4, True), (3, True), (3, False)])
+def test_offloaded_caches_match_resident(cuda, port, layers, prod):
+    """Cache offload (memory.cpp:33-58: two layers' caches on the device, the rest in host
+    memory, streamed per layer) runs the same kernels on the same data, so the generated
+    latent must be BIT-identical to the all-resident run -- PROD with CUDA graphs (the
+    captured step includes the copy-stream traffic) and CHECK eagerly, even and odd stacks."""
+    import torch
+    from paper_2506_03275_b200 import ops
+    n, d, hh, e, f, c = 512, 256, 4, 64, 1024, 64
+    std = 1 / np.sqrt(d)
+    cfg = ops.BlockConfig(batch=1, seq=n, dim=d, heads=hh, head_dim=e, hidden=f, chunk=c,
+                          attn_k=64, mlp_k=128)
+
+    def weights(l):
+        base = 100 * (l + 1)
+        return {"wq": port.gaussian(base + 1, (d, d), std), "wk": port.gaussian(base + 2, (d, d), std),
+                "wv": port.gaussian(base + 3, (d, d), std), "wo": port.gaussian(base + 4, (d, d), std / 2),
+                "w1": port.gaussian(base + 5, (f, d), std), "b1": port.gaussian(base + 6, (f,), std),
+                "w2": port.gaussian(base + 7, (f, d), std / 2), "b2": port.gaussian(base + 8, (d,), std / 2)}
+    ws = [weights(l) for l in range(layers)]
+    layout = ops.VoxelLayout(1, 16, 32, 1, 8, 8)
+    grid0 = torch.as_tensor(port.gaussian(77, (1, 1, 16, 32, d))).cuda().to(torch.bfloat16).float()
+    sched = G.ScheduleParams(total_steps=7, dense_interval=2, step_cache=True, window=3, stride=2)
+    finals, mems = {}, {}
+    for off in (False, True):
+        gen = G.Generation([ops.Block(cfg, w, production=prod) for w in ws], layout, offload=off)
+        assert gen.offload == off
+        rep = gen.run(grid0, sched)
+        finals[off] = rep.final_latent.cpu()
+        mems[off] = gen.memory_report()
+    assert torch.equal(finals[True], finals[False])
+    assert mems[True]["cache_device_bytes"] * layers == 2 * mems[False]["cache_device_bytes"]
