@@ -249,7 +249,10 @@ csd_status csd_block_destroy(csd_block* blk);
  * and computes its column sums with fresh softmax stats. */
 csd_status csd_block_reset(csd_block* blk);
 /* model_forward_step for one layer: x_out = block(x_in).  x in the mode's
- * activation dtype, [B,N,D] device.  dense != 0 refreshes the caches.
+ * activation dtype, [B,N,D] device.  dense = 1 refreshes the caches; dense = 2 is
+ * model_forward_dense (model.cpp:167-176): exact attention + dense MLP, the caches left
+ * untouched (the dense baseline trajectory; scratch allocated on first use, so run it once
+ * outside a graph capture first).
  * static_idx/static_counts (nullable, device) replace the attention top-k
  * on dense steps (attention.hpp:50-52): int32 [B, heads_local, N/chunk, static_k_max]
  * and [B, heads_local, N/chunk], static_k_max == cfg.attn_k.  The pattern is validated

@@ -55,6 +55,9 @@ struct csd_block {
     float* mout = nullptr;
     int32_t *midx = nullptr, *mcnt = nullptr;
     bool attn_init = false, mlp_init = false;
+    // scratch of the cache-free dense forward (CSD_BLOCK_FORWARD_DENSE), allocated on first use
+    void* plain_act = nullptr;
+    float* plain_mout = nullptr;
     int64_t attn_age = 0, mlp_age = 0;
     // the MLP's view of the rows: (batch, seq) of the block, or (1, t_local) when token-sharded
     int64_t mB = 0, mN = 0;
@@ -284,8 +287,19 @@ csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int den
     csd_ctx* ctx = reinterpret_cast<csd_ctx*>(blk->ctx);
     const csd_mode md = blk->mode;
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (dense < 0 || dense > 2) return set_error(CSD_ERR_VALUE, "step kind %d (0 sparse, 1 dense, 2 forward-dense)", dense);
+    const bool plain = dense == 2;
     if (!dense && (!blk->attn_init || !blk->mlp_init))
         return set_error(CSD_ERR_STATE, "sparse attention step requested before any dense step");
+    if (plain && static_idx)
+        return set_error(CSD_ERR_VALUE, "the cache-free dense forward takes no attention pattern");
+    if (plain && !blk->plain_act) {  // first use (eager, before any graph capture of it)
+        blk->plain_act = blk->alloc(esz(md) * c.batch * c.seq * c.f_local);
+        blk->plain_mout = static_cast<float*>(blk->alloc(4 * c.batch * c.seq * c.dim));
+        if (!blk->plain_act || !blk->plain_mout) return set_error(CSD_ERR_CUDA, "forward-dense scratch allocation failed");
+    }
+    void* const act = plain ? blk->plain_act : blk->act;
+    float* const mout = plain ? blk->plain_mout : blk->mout;
     if (dense && static_idx) {
         // A caller-supplied static pattern (attention.cpp:205-213) is checked BEFORE anything
         // runs, so a bad pattern leaves every cache untouched (as the reference, which throws
@@ -332,6 +346,11 @@ csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int den
         // ---- MLP branch; x2 = x1 + M is fused into the last MLP kernel's epilogue.  With
         // mlp_k >= F every neuron is recomputed on a sparse step (mlp.cpp:120-182 with the full
         // index set), which is the dense MLP with the cache refreshed (WAN-style configs)
+        if (plain) {  // dense MLP into scratch: the caches stay as the last dense step left them
+            CSD_TRY(csd::prod_dense_mlp(blk->ctx, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B,
+                                        N, D, Fl, c.chunk, mout, act, blk->x_mid, x_out, s));
+            return CSD_OK;
+        }
         if (dense || mk >= Fl) {
             CSD_TRY(csd::prod_dense_mlp(blk->ctx, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B,
                                         N, D, Fl, c.chunk, blk->mout, blk->act, blk->x_mid, x_out,
@@ -351,6 +370,11 @@ csd_status csd_block_step(csd_block* blk, const void* x_in, void* x_out, int den
     // ---------------- CHECK mode: op for op as model.cpp:200-213
     CSD_TRY(csd_project(ctx, md, blk->attn, blk->wo, B, N, Dl, D, blk->proj, stream));
     CSD_TRY(csd_add(ctx, md, x_in, blk->proj, B * N * D, blk->x_mid, stream));
+    if (plain) {
+        CSD_TRY(csd_dense_mlp(ctx, md, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B, N, D, Fl,
+                              c.chunk, mout, act, stream));
+        return csd_add(ctx, md, blk->x_mid, mout, B * N * D, x_out, stream);
+    }
     if (dense) {
         CSD_TRY(csd_dense_mlp(ctx, md, blk->x_mid, blk->w1, blk->b1, blk->w2, blk->b2, B, N, D, Fl,
                               c.chunk, blk->mout, blk->act, stream));
@@ -394,6 +418,10 @@ static csd_status attn_core(csd_block* blk, const void* x_in, int dense, const i
         CSD_TRY(csd_project(ctx, md, x_in, blk->wq, B, N, D, Dl, blk->q, stream));
         CSD_TRY(csd_project(ctx, md, x_in, blk->wk, B, N, D, Dl, blk->k, stream));
         CSD_TRY(csd_project(ctx, md, x_in, blk->wv, B, N, D, Dl, blk->v, stream));
+    }
+    if (dense == 2) {  // model_forward_dense (model.cpp:167-176): exact attention, no caches
+        return csd_dense_attention(ctx, md, CSD_LAYOUT_BNHE, blk->q, blk->k, blk->v, B, Hl, N, E,
+                                   blk->attn, stream);
     }
     // Index sets produced inside the block are valid by construction (top-k); a static
     // pattern was validated by csd_block_step before anything ran.  Skip per-call validation.

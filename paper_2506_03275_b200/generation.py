@@ -234,7 +234,7 @@ class Generation:
         for _ in range(total):
             cur = shadow if self.prod else lat
             for blk, out in zip(self.baseline, outs):
-                blk.step(cur, True, out=out)  # a dense step: exact attention and MLP
+                blk.forward_dense(cur, out=out)  # model_forward_dense: exact attention + MLP
                 cur = out
             latent_axpy(lat, scale, outs[-1], shadow if self.prod else None)
             traj.append(lat.clone())

@@ -549,6 +549,17 @@ class Block:
             static.k_max if static else 0, _stream()))
         return out
 
+    def forward_dense(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """model_forward_dense for this layer (model.cpp:167-176): exact attention + dense MLP,
+        no cache touched (the reference's dense baseline)."""
+        if x.dtype != self.dtype:
+            raise TypeError(f"block expects {self.dtype} activations")
+        if out is None:
+            out = torch.empty_like(x)
+        raise_for(self.ctx.lib, self.ctx.lib.csd_block_step(self.h, _ptr(x), _ptr(out), 2, None, None, 0,
+                                                             _stream()))
+        return out
+
     def reset(self):
         """A fresh ModelState for this layer (model.cpp:101-105): the next step must be dense."""
         raise_for(self.ctx.lib, self.ctx.lib.csd_block_reset(self.h))

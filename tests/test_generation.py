@@ -160,3 +160,37 @@ def test_offloaded_caches_match_resident(cuda, port, layers, prod):
         mems[off] = gen.memory_report()
     assert torch.equal(finals[True], finals[False])
     assert mems[True]["cache_device_bytes"] * layers == 2 * mems[False]["cache_device_bytes"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prod", [True, False])
+def test_forward_dense_equals_dense_step_output(cuda, port, prod):
+    """model_forward_dense (csd_block_step kind 2): the output of a Chipmunk dense step (the
+    exact attention and MLP the caches are refreshed from), with every cache left untouched."""
+    import torch
+    from paper_2506_03275_b200 import ops
+    n, d, hh, e, f, c = 512, 256, 4, 64, 1024, 64
+    std = 1 / np.sqrt(d)
+    w = {"wq": port.gaussian(1, (d, d), std), "wk": port.gaussian(2, (d, d), std),
+         "wv": port.gaussian(3, (d, d), std), "wo": port.gaussian(4, (d, d), std / 2),
+         "w1": port.gaussian(5, (f, d), std), "b1": port.gaussian(6, (f,), std),
+         "w2": port.gaussian(7, (f, d), std / 2), "b2": port.gaussian(8, (d,), std / 2)}
+    cfg = ops.BlockConfig(batch=1, seq=n, dim=d, heads=hh, head_dim=e, hidden=f, chunk=c,
+                          attn_k=64, mlp_k=128)
+    blk = ops.Block(cfg, w, production=prod)
+    dt = torch.bfloat16 if prod else torch.float32
+    x = torch.as_tensor(port.gaussian(9, (1, n, d))).cuda().to(dt)
+    x2 = torch.as_tensor(port.gaussian(10, (1, n, d))).cuda().to(dt)
+    y_dense = blk.step(x, True)
+    caches = [blk.cache(i) for i in range(6)] + list(blk.indices(False)) + list(blk.indices(True))
+    y_plain = blk.forward_dense(x2)  # a different input: the caches must not move
+    after = [blk.cache(i) for i in range(6)] + list(blk.indices(False)) + list(blk.indices(True))
+    for a, b in zip(caches, after):
+        assert torch.equal(a, b)
+    y_plain_x = blk.forward_dense(x)
+    if prod:  # same kernels except the attention pass (dense vs column-sum): bf16 contract
+        err = float((y_plain_x.float() - y_dense.float()).norm() / y_dense.float().norm())
+        assert err < 1e-2, err
+    else:
+        assert torch.equal(y_plain_x, y_dense)
+    assert not torch.equal(y_plain, y_plain_x)
