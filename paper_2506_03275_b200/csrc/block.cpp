@@ -491,7 +491,7 @@ static csd_status sparse_mlp_apply(csd_block* blk, const void* x_mid, void* x_ou
     const int64_t mk = c.mlp_k > 0 ? c.mlp_k : Fl;
     if (!mlp_tc_supported(D, c.chunk))
         return set_error(CSD_ERR_UNSUPPORTED, "sparse-delta MLP envelope (D %% 128, chunk <= 256)");
-    const int64_t k_pad = csd::dev::prod_smlp_delta_cols(mk, B * (N / c.chunk));
+    const int64_t k_pad = csd::dev::prod_smlp_delta_cols(mk, B * (N / c.chunk), c.chunk);
     void* dws = blk->ctx->ws(csd::kWsDelta, 2 * B * N * k_pad, s);
     if (!dws) return set_error(CSD_ERR_CUDA, "workspace allocation failed");
     CSD_CU(prod_sparse_delta_mlp_tc(x_mid, blk->w1, blk->b1, blk->w2, blk->midx, blk->mcnt, mk,

@@ -398,7 +398,7 @@ csd_status csd_sparse_delta_mlp(csd_ctx* ctx, csd_mode mode, const void* x, cons
             return set_error(CSD_ERR_UNSUPPORTED,
                              "production sparse-delta MLP needs model_dim %% 128 == 0 and chunk <= 256 "
                              "(got D=%lld, chunk=%lld)", (long long)d, (long long)chunk);
-        const int64_t k_pad = csd::dev::prod_smlp_delta_cols(k_max, rows);
+        const int64_t k_pad = csd::dev::prod_smlp_delta_cols(k_max, rows, chunk);
         void* dws = c->ws(csd::kWsDelta, 2 * rows * chunk * (k_pad ? k_pad : 128), s);
         CSD_TRY(need_ws(dws));
         CSD_CU(prod_sparse_delta_mlp_tc(x, w1, b1, w2, idx, counts, k_max, chunk, batch, n, d, f,

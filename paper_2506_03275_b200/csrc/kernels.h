@@ -168,7 +168,7 @@ cudaError_t prod_add_bf16_f32(const void* a, const float* b, int64_t numel, void
                               cudaStream_t s);// mlp_tc.cu: delta_ws >= B*C*chunk*round_up(k_max,128) bf16
 bool mlp_tc_supported(int64_t d, int64_t chunk);
 // delta-workspace columns (k_pad) the tcgen05 sparse-delta MLP uses for k_max / nz chunks
-int64_t prod_smlp_delta_cols(int64_t k_max, int64_t nz);
+int64_t prod_smlp_delta_cols(int64_t k_max, int64_t nz, int64_t chunk);
 cudaError_t prod_sparse_delta_mlp_tc(const void* x, const void* w1, const float* b1,
                                      const void* w2, const int32_t* idx, const int32_t* counts,
                                      int64_t k_max, int64_t chunk, int64_t batch, int64_t n,

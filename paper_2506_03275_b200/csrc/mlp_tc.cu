@@ -127,7 +127,7 @@ __device__ __forceinline__ void mlp_setup(uint8_t* smem, uint64_t*& full, uint64
 // Tile = (chunk z, neuron tile tn of TN = p.tn_width neurons; TN is picked on the host so
 // that all tiles run in ONE wave on 148 SMs, e.g. FLUX 860 -> 6 x 144).  MMA: M = chunk
 // rows (NT x 128), N = TN, K = D.  Stage = x tile (TMA) + TN gathered W1 k-slices (cp.async).
-constexpr int kUpMaxTN = 192;
+constexpr int kUpMaxTN = 240;  // TMEM: NT x 240 <= 512 columns; see smlp_geometry for the smem cap
 template <int NT>
 struct UpLayout {
     static constexpr uint32_t kStageMax = NT * kTile + kUpMaxTN * 128;
@@ -673,7 +673,7 @@ bool mlp_tc_supported(int64_t d, int64_t chunk) {
     return d % 128 == 0 && chunk >= 8 && chunk <= 256 && chunk % 8 == 0;
 }
 
-void smlp_geometry(int64_t k_max, int64_t nz, int* tn_width, int* ntiles, int64_t* k_pad);
+void smlp_geometry(int64_t k_max, int64_t nz, int64_t chunk, int* tn_width, int* ntiles, int64_t* k_pad);
 
 template <int NT>
 static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, const void* w2,
@@ -685,7 +685,7 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
     using LU = UpLayout<NT>;
     const int64_t nc = n / chunk;
     int tn_width = 0, ntiles = 0;
-    smlp_geometry(k_max, batch * nc, &tn_width, &ntiles, nullptr);
+    smlp_geometry(k_max, batch * nc, chunk, &tn_width, &ntiles, nullptr);
     CUtensorMap tx, tdl, tmc, txm, txo;
     const uint64_t rows_all = (uint64_t)(batch * n);
     if (!make_map_bf16(&tx, x, d, batch * n, d, 64) ||
@@ -734,22 +734,40 @@ static cudaError_t launch_smlp(const void* x, const void* w1, const float* b1, c
 // (FLUX: 24 chunks -> 6 tiles of 144 for k = 860), width a multiple of 16 in [64, 192].
 // The delta workspace is [B*C*chunk rows][k_pad] bf16, k_pad = round_up(tiles * width, 64)
 // (the down GEMM's 64-neuron k-blocks read up to round_up(count, 64) columns).
-void smlp_geometry(int64_t k_max, int64_t nz, int* tn_width, int* ntiles, int64_t* k_pad) {
+void smlp_geometry(int64_t k_max, int64_t nz, int64_t chunk, int* tn_width, int* ntiles, int64_t* k_pad) {
     const int sms = sm_count();
     const int64_t km = std::max<int64_t>(k_max, 1);
     const int64_t fit = std::max<int64_t>(1, sms / std::max<int64_t>(nz, 1));
+    // widest tile: its epilogue stages the activation tile [TN][chunk] and the delta tile
+    // [chunk][TN + 8] (bf16) in the idle stage ring, which must hold them
+    auto staging_fits = [&](int64_t w) {
+        const int nt = chunk > 128 ? 2 : 1;
+        const int64_t stage = nt * (int64_t)kTile + w * 128;
+        const int64_t ring = (4 * stage + 128 + 2048 + 1024 <= 227 * 1024 ? 4 : 3) * stage;
+        const int64_t need = ((w * chunk * 2 + 1023) / 1024) * 1024 + chunk * (w * 2 + 16);
+        return need <= ring;
+    };
+    int64_t wmax = 192;  // the round-1 envelope: always fits
+    for (int64_t w = kUpMaxTN; w > 192; w -= 16)
+        if (staging_fits(w)) {
+            wmax = w;
+            break;
+        }
     int64_t w = (km + fit - 1) / fit;
     w = (w + 15) / 16 * 16;
-    w = std::min<int64_t>(std::max<int64_t>(w, 64), kUpMaxTN);
+    // one wave at <= wmax neurons per tile; past that the tiles run in several waves anyway
+    // and the narrower 192 measured faster (FLUX 85 %: 186 vs 200 us)
+    w = std::max<int64_t>(w, 64);
+    if (w > wmax) w = 192;
     const int64_t t = (km + w - 1) / w;
     if (tn_width) *tn_width = (int)w;
     if (ntiles) *ntiles = (int)t;
     if (k_pad) *k_pad = (t * w + 63) / 64 * 64;
 }
 
-int64_t prod_smlp_delta_cols(int64_t k_max, int64_t nz) {
+int64_t prod_smlp_delta_cols(int64_t k_max, int64_t nz, int64_t chunk) {
     int64_t k_pad = 0;
-    smlp_geometry(k_max, nz, nullptr, nullptr, &k_pad);
+    smlp_geometry(k_max, nz, chunk, nullptr, nullptr, &k_pad);
     return k_pad;
 }
 
@@ -762,7 +780,7 @@ cudaError_t prod_sparse_delta_mlp_tc(const void* x, const void* w1, const float*
     if (!mlp_tc_supported(d, chunk)) return cudaErrorNotSupported;
     if (k_max == 0) return cudaSuccess;
     int64_t k_pad = 0;
-    smlp_geometry(k_max, batch * (n / chunk), nullptr, nullptr, &k_pad);
+    smlp_geometry(k_max, batch * (n / chunk), chunk, nullptr, nullptr, &k_pad);
     if (chunk > 128)
         return launch_smlp<2>(x, w1, b1, w2, idx, counts, k_max, chunk, batch, n, d, f, act_cm,
                               out_cache, delta_ws, k_pad, s, x_mid, x_out);
