@@ -134,7 +134,10 @@ __device__ __forceinline__ uint64_t pp_globaltimer() {
 // kOrd: the launch carries an LPT item order (p.order).  Without it the order indirection is
 // compiled out: a kernel-wide order pointer is otherwise spilled (128-register launch bound)
 // and reloaded from local memory at every item lookup.
-template <int E, int kPoly, bool kOrd>
+// kDense: dense passes (all keys by TMA tiles) vs sparse items (gathered K/V rows); a
+// compile-time split so each instance carries only its own code (instruction fetch is a
+// measured cost of this kernel: the cold first item after the Q/K/V GEMM)
+template <int E, int kPoly, bool kOrd, bool kDense>
 __global__ void __launch_bounds__(PPLayout<E>::kThreads, 1)
 k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
           const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_b,
@@ -146,7 +149,7 @@ k_attn_pp(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
     uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool dense = p.idx == nullptr;
+    constexpr bool dense = kDense;
     const int items = p.items;
     if (threadIdx.x == 0 && p.span != nullptr) p.span[2 * blockIdx.x] = pp_globaltimer();
     if (threadIdx.x == 0) PP_TRACE(15, 0);
@@ -865,8 +868,10 @@ cudaError_t launch_pp(const AttnTcArgs& a, cudaStream_t s) {
         return e ? std::atoi(e) : -1;
     }();
     const int poly = poly_env >= 0 ? poly_env : (a.idx == nullptr ? 4 : 0);
-    auto kern = a.order != nullptr ? (poly == 4 ? k_attn_pp<E, 4, true> : k_attn_pp<E, 0, true>)
-                                   : (poly == 4 ? k_attn_pp<E, 4, false> : k_attn_pp<E, 0, false>);
+    // dense passes: poly 4 by default, no LPT order; sparse items: poly 0, LPT order optional
+    auto kern = a.idx == nullptr ? (poly == 4 ? k_attn_pp<E, 4, false, true> : k_attn_pp<E, 0, false, true>)
+                : a.order != nullptr ? (poly == 4 ? k_attn_pp<E, 4, true, false> : k_attn_pp<E, 0, true, false>)
+                                     : (poly == 4 ? k_attn_pp<E, 4, false, false> : k_attn_pp<E, 0, false, false>);
     cudaError_t err = ensure_smem_attr(kern, (int)L::kMaxSmem);
     if (err != cudaSuccess) return err;
     const unsigned grid = (unsigned)std::min<int64_t>(p.items, sm_count());
