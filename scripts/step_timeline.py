@@ -23,10 +23,15 @@ def main():
     ap.add_argument("--kind", default="sparse", choices=["sparse", "dense"])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--out", default="")
+    ap.add_argument("--hunyuan", action="store_true",
+                    help="the HunyuanVideo-shaped block (configs[3]: 118272 tokens, 95 %%)")
     args = ap.parse_args()
     cfg = dict(bench.FLUX)
     n = cfg["grid"][1] * cfg["grid"][2]
-    ak, mk = bench.k_of(n, cfg["sparsity"]), bench.k_of(cfg["hidden"], cfg["sparsity"])
+    sp = cfg["sparsity"]
+    if args.hunyuan:
+        n, sp = 32 * 42 * 88, 0.95
+    ak, mk = bench.k_of(n, sp), bench.k_of(cfg["hidden"], sp)
     bc = ops.BlockConfig(batch=1, seq=n, dim=cfg["dim"], heads=cfg["heads"],
                          head_dim=cfg["head_dim"], hidden=cfg["hidden"], chunk=cfg["chunk"],
                          attn_k=ak, mlp_k=mk)
@@ -55,7 +60,7 @@ def main():
             torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     evs.sort(key=lambda e: e.time_range.start)
-    # split into replays at gaps > 20 us
+    # split into replays at gaps > 20 us (long steps: one replay per synchronize anyway)
     reps, cur = [], []
     for e in evs:
         if cur and e.time_range.start - cur[-1].time_range.end > 20:
