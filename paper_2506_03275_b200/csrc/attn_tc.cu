@@ -1019,6 +1019,7 @@ cudaError_t attn_tc(const AttnTcArgs& a, cudaStream_t s) {
     if (!attn_tc_supported(a.e, a.chunk)) return cudaErrorNotSupported;
     if (a.n % a.chunk) return cudaErrorInvalidValue;
     if (attn_sd_supported(a)) return attn_sd(a, s);
+    if (attn_px_supported(a)) return attn_px(a, s);
     if (attn_cp_supported(a)) return attn_cp(a, s);
     if (attn_pp_supported(a)) return attn_pp(a, s);
     const bool two = a.chunk > 128;

@@ -120,6 +120,10 @@ cudaError_t attn_pp(const AttnTcArgs& a, cudaStream_t s);
 // attn_cp.cu: sparse delta attention on CTA pairs (chunk 192 / 256, E 128, with base);
 // attn_tc() dispatches to it before the ping-pong kernel (CSD_ATTN_CP=0 turns it off).
 bool attn_cp_supported(const AttnTcArgs& a);
+// attn_px.cu: the ping-pong kernel with P staged in shared memory (SS-form P V, the S buffer
+// released as soon as it is in registers); opt-in (CSD_ATTN_PX=1) while measured.
+bool attn_px_supported(const AttnTcArgs& a);
+cudaError_t attn_px(const AttnTcArgs& a, cudaStream_t s);
 cudaError_t attn_cp(const AttnTcArgs& a, cudaStream_t s);
 
 // gemm_tc.cu: persistent tcgen05 GEMMs with fused epilogues (projections, dense MLP).

@@ -290,20 +290,30 @@ def test_prod_sparse_delta_attention(ops, port, e, chunk, n, layout, h):
             idx[0, hh, c, :m] = rng.permutation(n)[:m]
             cnt[0, hh, c] = m
     to_bhne = (lambda a: a) if layout == 0 else (lambda a: np.ascontiguousarray(a.transpose(0, 2, 1, 3)))
-    # chunk 192 / 256 with E 128 also runs through the opt-in CTA-pair kernel (attn_cp.cu)
-    pair_modes = (0, 1) if (e == 128 and chunk in (192, 256)) else (0,)
+    # chunk 192 / 256 with E 128 also runs through the opt-in CTA-pair kernel (attn_cp.cu, mode
+    # 1) and chunk 192 through the P-in-shared-memory kernel (attn_px.cu, mode 2)
+    modes = (0,)
+    if e == 128 and chunk in (192, 256):
+        modes = (0, 1, 2) if chunk == 192 else (0, 1)
     from paper_2506_03275_b200 import _capi
     set_cp = _capi.lib().csd_debug_set_attn_cp
-    for scale, pair in [(sc, pm) for sc in (1.0, -1.0) for pm in pair_modes]:
+    set_px = _capi.lib().csd_debug_set_attn_px
+    for scale, mode in [(sc, md) for sc in (1.0, -1.0) for md in modes]:
         want = port.sparse_delta_attention(to_bhne(q16), to_bhne(k16), to_bhne(v16), idx, cnt, chunk,
                                            to_bhne(b16), scale)
-        set_cp(pair)
+        set_cp(int(mode == 1))
+        set_px(int(mode == 2))
+        # the px kernel runs only in identity item order (no LPT)
+        ctx = ops.context()
+        ctx.lib.csd_ctx_set_lpt(ctx.h, int(mode != 2))
         try:
             got = ops.sparse_delta_attention(T(q16, torch.bfloat16), T(k16, torch.bfloat16),
                                              T(v16, torch.bfloat16), index_set(ops, idx, cnt, chunk, n),
                                              T(b16, torch.bfloat16), scale, layout=layout)
         finally:
             set_cp(0)
+            set_px(0)
+            ctx.lib.csd_ctx_set_lpt(ctx.h, 1)
         got = to_bhne(N(got))
         # delta part only (base cancels) must match to bf16 accuracy
         err = rel_l2(got - to_bhne(b16), want - to_bhne(b16))
