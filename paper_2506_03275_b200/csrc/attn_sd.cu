@@ -368,10 +368,13 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                 const float neg_m = row_ok ? -m_run : -INFINITY;
                 const float2 sl2v = make_float2(sl2, sl2), nm2 = make_float2(neg_m, neg_m);
                 float2 part0 = make_float2(0.f, 0.f), part1 = make_float2(0.f, 0.f);
-                if (kCs && g >= 1) mbar_wait(bar_cs + ((g - 1) & 1), ((g - 1) >> 1) & 1);  // P/W smem free
+                // P of both 32-key groups stays in registers until the smem copy (kCs): the
+                // wait for the previous block's column-sum MMA (P / W smem free) comes after the
+                // exponentials instead of before them
+                uint32_t pka[32];
 #pragma unroll
                 for (int cc = 0; cc < 2; ++cc) {
-                    uint32_t pk[16];
+                    uint32_t(&pk)[16] = *reinterpret_cast<uint32_t(*)[16]>(&pka[cc * 16]);
                     if (cc * 32 >= nh) {
 #pragma unroll
                         for (int q = 0; q < 16; ++q) pk[q] = 0u;
@@ -394,20 +397,17 @@ k_attn_sd(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUte
                         }
                     }
                     tmem_st16(tS + hf * 32 + cc * 16, pk);  // P of keys 64 hf + 32 cc ..
-                    if (kCs) {
-                        // the row's P copy (K-major, 128B-swizzled): strip hf, chunks cc * 4 ..
-                        uint8_t* rp = sp + hf * L::kStrip + row * 128;
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int ch = cc * 4 + u;
-                            *reinterpret_cast<uint4*>(rp + ((ch ^ (row & 7)) << 4)) =
-                                make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-                        }
-                    }
                 }
                 const float2 part = __fadd2_rn(part0, part1);
                 l_run += part.x + part.y;
                 if (kCs) {
+                    if (g >= 1) mbar_wait(bar_cs + ((g - 1) & 1), ((g - 1) >> 1) & 1);  // P/W smem free
+                    // the row's P copy (K-major, 128B-swizzled): strip hf, 16-byte chunks 0..7
+                    uint8_t* rp = sp + hf * L::kStrip + row * 128;
+#pragma unroll
+                    for (int ch = 0; ch < 8; ++ch)
+                        *reinterpret_cast<uint4*>(rp + ((ch ^ (row & 7)) << 4)) =
+                            make_uint4(pka[4 * ch], pka[4 * ch + 1], pka[4 * ch + 2], pka[4 * ch + 3]);
                     if (hf == 0) {
                         // W[slot][row] = w, W[1 - slot][row] = 0 (bf16, K-major 128B-swizzled).
                         // Stale stats far below the fresh logits: the reference's fp32 exp
