@@ -25,6 +25,8 @@ using namespace csd::tc;
 // mode 10: mode 1 (TS) while 8 warps stream 16-byte smem stores
 // mode 11: mode 5 while 8 warps stream TMEM loads + stores on other columns (softmax-like)
 // mode 12: mode 5 while 8 warps load / store the columns the MMAs use (as the softmax does)
+// modes 13-17: SS with other M / N (the sparse MLP's tile shapes): M64 N128, M128 N144,
+//              M64 N144, M128 N192, M64 N192
 template <int MODE>
 __global__ void __launch_bounds__(384, 1) k_mma_rate(long long* out, int groups) {
     extern __shared__ uint8_t smem_raw[];
@@ -51,8 +53,10 @@ __global__ void __launch_bounds__(384, 1) k_mma_rate(long long* out, int groups)
     constexpr uint32_t kStrip = 128 * 128;
     long long t0 = 0, t1 = 0;
     if (warp == 0) {
-        const uint32_t n = MODE == 2 ? 256 : MODE == 3 ? 64 : 128;
-        const uint32_t idSS = idesc_bf16(128, n, false, false);
+        const uint32_t n = MODE == 2 ? 256 : MODE == 3 ? 64 : (MODE == 14 || MODE == 15) ? 144
+                         : (MODE == 16 || MODE == 17) ? 192 : 128;
+        const uint32_t m = (MODE == 13 || MODE == 15 || MODE == 17) ? 64 : 128;
+        const uint32_t idSS = idesc_bf16(m, n, false, false);
         const uint32_t idSSmn = idesc_bf16(128, 128, false, true);
         uint64_t da[8], db[8], dbm[8];
 #pragma unroll
@@ -170,6 +174,11 @@ int main() {
     run<10>("TS + 8 warps streaming smem stores", d, f128);
     run<11>("S/PV + 8 warps TMEM ld/st on other columns", d, f128);
     run<12>("S/PV + 8 warps TMEM loads of the MMA columns", d, f128);
+    run<13>("SS M64 N128 K16", d, f128 / 2);
+    run<14>("SS M128 N144 K16", d, f128 * 144 / 128);
+    run<15>("SS M64 N144 K16", d, f128 * 144 / 256);
+    run<16>("SS M128 N192 K16", d, f128 * 192 / 128);
+    run<17>("SS M64 N192 K16", d, f128 * 192 / 256);
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
