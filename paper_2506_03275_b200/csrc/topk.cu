@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "launch_util.h"
+#include "tc_common.cuh"
 
 namespace csd {
 namespace dev {
@@ -281,14 +282,27 @@ k_topk_rows(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* __r
 // per-CTA / per-warp counts above the selected digit accumulate into exact gt / eq offsets,
 // so one write pass emits the index SET (strictly greater, then the lowest-index ties), each
 // part in index order.  Unsorted output only (the PROD block path).
-__device__ __forceinline__ uint32_t dsmem_ld(const uint32_t* local_addr, uint32_t cta) {
-    uint32_t raddr, v;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(smem_u32_generic(local_addr)), "r"(cta));
-    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(raddr) : "memory");
-    return v;
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t local, uint32_t cta) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(cta));
+    return r;
+}
+// Remote shared-memory stores that complete_tx on the receiver's mbarrier: the histogram
+// exchange needs no cluster-wide barrier (barrier.cluster.arrive.release compiles to
+// MEMBAR.ALL.GPU + CCTL.IVALL per pass)
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, uint4 v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+                 ::"r"(raddr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, uint32_t a, uint32_t b, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];"
+                 ::"r"(raddr), "r"(a), "r"(b), "r"(rbar) : "memory");
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -311,8 +325,11 @@ k_topk_cluster(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* 
     extern __shared__ __align__(16) uint8_t smem[];
     uint32_t* keys = reinterpret_cast<uint32_t*>(smem);  // this CTA's segment
     __shared__ uint32_t whist[kTopkWarps][256];
-    __shared__ uint32_t chist[2][256];        // this CTA's histogram, double-buffered by pass
-    __shared__ uint32_t red[2];               // AND / OR of this CTA's keys
+    // every CTA's histogram, double-buffered by pass: slot [rank] written locally, the peers'
+    // slots by their st.async pushes (mb[pass & 1]); AND / OR of the keys likewise (mb[2])
+    __shared__ __align__(16) uint32_t rhist[2][CS][256];
+    __shared__ __align__(8) uint32_t rred[CS][2];
+    __shared__ __align__(8) uint64_t mb[3];
     __shared__ uint32_t s_prefix, s_kleft, s_sel, s_shift;
     __shared__ uint32_t cta_gt[CS], warp_gt[kTopkWarps], warp_eq[kTopkWarps], cta_eq[CS];
     __shared__ uint32_t tot_bins[256];
@@ -320,6 +337,11 @@ k_topk_cluster(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* 
     if (threadIdx.x == 0) pdl_trigger();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t rank = cluster_rank();
+    if (tid == 0) {
+        for (int i = 0; i < 3; ++i) tc::mbar_init(&mb[i], 1);
+        tc::fence_barrier_init();
+    }
+    cluster_arrive_relaxed();  // waited for after the load phase: the peers' barriers exist
     const int64_t row = blockIdx.x / CS;
     const float* src = scores + row * m;
     TOPK_TRACE(0);
@@ -371,16 +393,19 @@ k_topk_cluster(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* 
     if (tid < CS) { cta_gt[tid] = 0; cta_eq[tid] = 0; }
     if (tid < kTopkWarps) warp_gt[tid] = 0;
     __syncthreads();
+    cluster_wait();
     if (tid == 0) {
         uint32_t a = 0xffffffffu, o = 0u;
         for (int w = 0; w < kTopkWarps; ++w) { a &= whist[0][w]; o |= whist[1][w]; }
-        red[0] = a;
-        red[1] = o;
-    }
-    cluster_sync_all();
-    if (tid == 0) {
-        uint32_t a = 0xffffffffu, o = 0u;
-        for (uint32_t r = 0; r < CS; ++r) { a &= dsmem_ld(&red[0], r); o |= dsmem_ld(&red[1], r); }
+        rred[rank][0] = a;
+        rred[rank][1] = o;
+        tc::mbar_arrive_expect_tx(&mb[2], (CS - 1) * 8);
+        for (uint32_t r = 1; r < CS; ++r) {
+            const uint32_t pr = (rank + r) % CS;
+            st_async_v2(mapa_u32(smem_u32_generic(&rred[rank][0]), pr), a, o, mapa_u32(smem_u32_generic(&mb[2]), pr));
+        }
+        tc::mbar_wait(&mb[2], 0);
+        for (uint32_t r = 0; r < CS; ++r) { a &= rred[r][0]; o |= rred[r][1]; }
         const int lead = __clz(a ^ o);
         s_prefix = lead >= 32 ? a : (a & ~(0xffffffffu >> lead));
         s_kleft = (uint32_t)k;
@@ -408,16 +433,27 @@ k_topk_cluster(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* 
             uint32_t acc = 0;
 #pragma unroll
             for (int w = 0; w < kTopkWarps; ++w) acc += whist[w][i];
-            chist[hb][i] = acc;
+            rhist[hb][rank][i] = acc;
         }
-        cluster_sync_all();  // every CTA's chist[hb] is final (and the peers' previous pass reads are done)
-        // thread = bin: its per-CTA counts (CS distributed-smem loads in flight) and the total
+        __syncthreads();
+        // push this CTA's histogram to the peers (64 x 16 B each); a peer is at most one pass
+        // ahead (it needs this CTA's push of the pass it is on), so two buffers suffice
+        if (tid == 0) tc::mbar_arrive_expect_tx(&mb[hb], (CS - 1) * 1024);
+        if (tid < 64 * (CS - 1)) {
+            const uint32_t pr = (rank + 1 + tid / 64) % CS;
+            const int q = tid % 64;
+            const uint4 v = *reinterpret_cast<const uint4*>(&rhist[hb][rank][q * 4]);
+            st_async_v4(mapa_u32(smem_u32_generic(&rhist[hb][rank][q * 4]), pr), v,
+                        mapa_u32(smem_u32_generic(&mb[hb]), pr));
+        }
+        tc::mbar_wait(&mb[hb], (pass >> 1) & 1);
+        // thread = bin: its per-CTA counts and the total
         uint32_t vr[CS];
         uint32_t vtot = 0;
         if (tid < 256) {
 #pragma unroll
             for (int r = 0; r < CS; ++r) {
-                vr[r] = dsmem_ld(&chist[hb][tid], (uint32_t)r);
+                vr[r] = rhist[hb][r][tid];
                 vtot += vr[r];
             }
             tot_bins[tid] = vtot;
@@ -508,7 +544,8 @@ k_topk_cluster(const float* __restrict__ scores, int64_t m, int64_t k, int32_t* 
     }
     if (rank == 0 && tid == 0 && counts) counts[row] = (int32_t)k;
     TOPK_TRACE(7);
-    cluster_sync_all();  // peers may still read this CTA's histograms / reductions
+    // no trailing cluster barrier: peers never read this CTA's shared memory, and every
+    // push this CTA receives has been waited for
 }
 
 // Fallback for k beyond the shared-memory sort: composites staged in global
