@@ -507,7 +507,9 @@ k_gemm2_tc(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUt
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(acc_empty + buf, 0);  // the leader's barrier
+            // the leader's barrier; release.cta is enough (the TMEM reads are waited and fenced),
+            // release.cluster would cost a MEMBAR.ALL.GPU behind the previous tile's stores
+            if (lane == 0) mbar_arrive_remote(acc_empty + buf, 0);
             gemm_epilogue<EPI, kChunks, BN>(p, mt * 256 + (int)rank * 128 + row, nt, half * (BN / 2), r);
         }
     }
